@@ -1,0 +1,136 @@
+/*
+ * hv.h — C ABI of the B200-native Gauss-Newton Hessian-vector-product library (libhv.so).
+ *
+ * What it computes (arxiv 2507.10804, PAPER.md; discrete readings in DESIGN.md §3):
+ *   forward   f(m) -> d       "values of u(x,t) at receiver locations"            PAPER.md:49 (§2)
+ *                              for (1/m^2) u_tt - lap u = s(t) delta(x - x_s)      PAPER.md:44-47 (Eq. equ:pde)
+ *   gradient  F* (f(m) - d)    misfit term of grad Phi, F = Born, F* = migration  PAPER.md:108-112 (Eq. equ:grad)
+ *   hessvec   H_d v = F* F v   misfit (Gauss-Newton) Hessian "accessed via matrix-vector products"
+ *                              "two wave equations per source"                      PAPER.md:9, 157-164 (§3)
+ *   psido     sum_k D_{a_k} F^-1 D_{b_k} F v  low-rank-symbol PsiDO apply          PAPER.md:240-247 (Eq. equ:lr-psido)
+ *                              (apply_psf / apply_pdo on assembled approximations)
+ *
+ * Discretisation (none is given by the paper; SURVEY.md §8(c) O1-O11 / DESIGN.md §3):
+ *   2-D constant-density acoustic u_tt = v^2 lap u + f, leapfrog in time, 8th-order 17-point Laplacian
+ *   (zero outside the padded grid), W-cell sponge with centred damping, point source s[n]/h^2, point receivers,
+ *   discretise-then-optimise exact adjoint, Gauss-Newton H_d = J^T J, Euclidean inner products, sigma = 1.
+ *
+ * Layout: every model-space array is [nz][nx] float32, z-major row-major (row iz, column ix), contiguous.
+ *         data arrays are [shot][nt][nrec] float32; probe batches are [K][nz][nx]; symbols are [r][nz][nx].
+ * Pointers: any array argument may be a HOST pointer or a DEVICE pointer of the context's device (the library
+ *         asks the CUDA runtime which). Host inputs are copied in and host outputs copied back inside the call.
+ *         Ownership stays with the caller; the library owns only its context workspace. Outputs are overwritten,
+ *         never accumulated into.
+ * Calls are blocking (they return when the result is complete) and are serialised per context; use one context
+ * per GPU. No call falls back to the CPU: without a usable sm_100a device hv_create fails with HV_ECUDA.
+ * Multi-GPU: each rank passes its shot shard [src_begin, src_end); gradient / hessvec return RANK-LOCAL partial
+ * sums over that shard (the per-source terms of PAPER.md:164); the caller all-reduces them (NCCL).
+ */
+#ifndef HV_H
+#define HV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HV_API __attribute__((visibility("default")))
+#else
+#define HV_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define HV_OK      0
+#define HV_EINVAL  1  /* bad argument: null pointer, index out of range, K < 1, r < 1, mode unknown      */
+#define HV_EGRID   2  /* array / grid shape does not match the configuration                             */
+#define HV_ECFL    3  /* dt * max(m) / h exceeds the stability limit 0.5546 (leapfrog + 8th order, 2-D)  */
+#define HV_ENOMEM  4  /* the plan exceeds the device-memory budget                                        */
+#define HV_ECUDA   5  /* CUDA / cuFFT error, or no sm_100 device                                          */
+#define HV_ESTATE  6  /* null / destroyed context                                                         */
+
+/* forward-history storage for the reverse pass (not in the paper) */
+#define HV_STORE_AUTO       0  /* FULL when it fits the budget, else CHECKPOINT                      */
+#define HV_STORE_FULL       1  /* keep the imaging factor (2 dt^2 / v) L u^n of every level in HBM    */
+#define HV_STORE_CHECKPOINT 2  /* keep (u^n, u^{n-1}) every ckpt_interval levels, replay segments      */
+
+typedef struct hv_ctx hv_ctx;
+
+typedef struct {
+  int32_t nz, nx;        /* interior grid (rows = depth), >= 1                                           */
+  float   h;             /* grid spacing [m]                                                             */
+  float   dt;            /* time step [s]                                                                */
+  int32_t nt;            /* time levels t_n = n dt, n = 0..nt-1, >= 3                                     */
+  int32_t sponge;        /* W: absorbing cells added on each side (>= 4)                                 */
+  float   v_ref;         /* fixed sponge reference speed [m/s]; eta_max = 3 v_ref ln(1e3) / (2 W h)       */
+  int32_t nsrc;          /* total shots; src_iz/src_ix: HOST arrays [nsrc], interior indices (copied)     */
+  const int32_t *src_iz, *src_ix;
+  int32_t nrec;          /* receivers (same for every shot); rec_iz/rec_ix: HOST arrays [nrec] (copied)   */
+  const int32_t *rec_iz, *rec_ix;
+  const float *wavelet;  /* HOST [nt]: source function s[n] (copied)                                     */
+  int32_t src_begin, src_end; /* this rank's shot shard [begin, end); end = 0 means nsrc                  */
+  int32_t store;         /* HV_STORE_*                                                                   */
+  int32_t ckpt_interval; /* CHECKPOINT spacing in levels; 0 = round(sqrt(nt))                            */
+  int32_t shot_batch;    /* shots propagated concurrently; 0 = auto from the memory budget               */
+  int32_t field_group;   /* Born / adjoint fields per CTA (tuning); 0 = auto                               */
+  int32_t device;        /* CUDA device ordinal                                                          */
+  size_t  mem_budget;    /* bytes of device memory the plan may use; 0 = 90 % of free memory             */
+} hv_config;
+
+/* Create / destroy. Validates geometry (indices inside the interior grid) -> HV_EINVAL. */
+HV_API int hv_create(const hv_config* cfg, hv_ctx** out);
+HV_API int hv_destroy(hv_ctx* ctx);
+
+/* Run subsequent work on this cudaStream_t (NULL = the context's own stream). */
+HV_API int hv_set_stream(hv_ctx* ctx, void* cuda_stream);
+
+/* d = f(m) for the shard's shots: m [nz][nx] (m/s); d [src_end - src_begin][nt][nrec]; d[:,0,:] = 0. */
+HV_API int hv_forward(hv_ctx* ctx, const float* m, float* d);
+
+/* Misfit gradient and value over the shard: d_obs [local shots][nt][nrec]; g [nz][nx];
+ * *phi = 1/2 sum (d - d_obs)^2 accumulated in float64 (phi may be NULL). */
+HV_API int hv_gradient(hv_ctx* ctx, const float* m, const float* d_obs, float* g, double* phi);
+
+/* Gauss-Newton H_d [v_1..v_K] over the shard: V, HV [K][nz][nx]. K >= 1. All K probes of a shot share one
+ * background wavefield (batched probing). */
+HV_API int hv_hessvec(hv_ctx* ctx, const float* m, int32_t K, const float* V, float* HV);
+
+/* Fused: gradient and K Hessian-vector products in one pass over the shard (1 + K fields forward,
+ * 1 + K adjoint fields backward). K >= 0. */
+HV_API int hv_gradient_hessvec(hv_ctx* ctx, const float* m, const float* d_obs, int32_t K, const float* V,
+                        float* g, double* phi, float* HV);
+
+/* Low-rank-symbol PsiDO apply on an nz x nx grid (Eq. equ:lr-psido):
+ *   mode 0: out = Re sum_k a_k . IDFT(b_k . DFT(v))
+ *   mode 1: out = Re sum_k IDFT(conj(b_k) . DFT(a_k . v))   (adjoint, Euclidean inner product)
+ *   mode 2: (mode 0 + mode 1) / 2                             (symmetrised)
+ * a [r][nz][nx] float32 (real spatial factors), b [r][nz][nx] interleaved complex64 (frequency factors at the
+ * unshifted DFT frequencies), v, out [nz][nx]. DFT unnormalised, IDFT scaled 1/(nz nx), so b == 1 is the
+ * identity. apply_psf == (a = PSF weights w_k, b = symbol rows); apply_pdo == (a = symbol columns, b = weights). */
+HV_API int hv_psido_apply(hv_ctx* ctx, int32_t nz, int32_t nx, int32_t r, const float* a, const float* b,
+                   const float* v, float* out, int32_t mode);
+
+/* Counters of the last call (for benches). */
+typedef struct {
+  int64_t kernel_launches;   /* launches of this library's kernels in the last call           */
+  int64_t graph_launches;    /* CUDA-graph replays in the last call                           */
+  int32_t shot_batch;        /* shots in flight used                                          */
+  int32_t field_group;       /* fields per CTA used                                           */
+  int32_t store;             /* storage mode used                                             */
+  int32_t ckpt_interval;
+  double  bytes_per_shot;    /* device bytes per shot in flight                               */
+  double  ms_forward;        /* device time of the forward sweeps (CUDA events), last call    */
+  double  ms_backward;       /* device time of the backward sweeps, last call                 */
+  double  ms_total;          /* device time of the whole call                                 */
+} hv_stats;
+HV_API int hv_get_stats(const hv_ctx* ctx, hv_stats* out);
+
+/* Human-readable detail of the last error on this context (never NULL). */
+HV_API const char* hv_last_error(const hv_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HV_H */

@@ -1,0 +1,607 @@
+// hv_api.cu — host runtime + C ABI of libhv.so (include/hv.h).
+//
+// Runtime responsibilities:
+//   - validate the configuration and geometry, precompute per-tile receiver lists;
+//   - plan a call: storage mode (FULL / CHECKPOINT), shots in flight, fields per CTA, within the HBM budget;
+//   - drive the time loops: forward sweep (fwd_step_kernel), checkpoint saves / segment replays, backward
+//     sweep (bwd_step_kernel), with per-sweep CUDA-event timing;
+//   - reduce the per-shot accumulators into the caller's outputs; host<->device staging when the caller
+//     passes host pointers.
+// Nothing here computes the method on the CPU: every step of the path runs in hv_kernels.cuh.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/hv.h"
+#include "hv_internal.h"
+#include "hv_kernels.cuh"
+
+using namespace hvk;
+using namespace hvrt;
+
+namespace {
+
+int make_tmap(hv_ctx* c, float* pool, long long nplanes, CUtensorMap* map) {
+  const Geo& g = c->g;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.Nx), static_cast<cuuint64_t>(g.Nz),
+                        static_cast<cuuint64_t>(nplanes)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.P) * 4, static_cast<cuuint64_t>(g.plane) * 4};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(HX), static_cast<cuuint32_t>(HZ), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = c->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, pool, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, HV_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return HV_OK;
+}
+
+int grid1d(long long n) { return static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16)); }
+
+// ------------------------------------------------------------------------------------------ the plan
+
+enum Want { W_FORWARD = 1, W_GRAD = 2, W_HESS = 4 };
+
+struct Plan {
+  int store = HV_STORE_FULL;
+  int k = 0;           // checkpoint interval
+  int nck = 0;         // checkpoints per shot
+  int S = 1;           // shots in flight
+  int FG = 8;
+  int nslot = 1;       // field slots per shot: 0 = background / residual adjoint, 1..K Born / adjoint, K+1 replay
+  int nacc = 0;        // accumulator slots
+  double per_shot = 0; // bytes
+};
+
+int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
+  const Geo& g = c->g;
+  const double F4 = 4.0;
+  const bool grad = want & W_GRAD;
+  const bool adjoint = want & (W_GRAD | W_HESS);
+  pl->nslot = 1 + K + (adjoint ? 1 : 0);  // + replay slot (CHECKPOINT)
+  pl->nacc = adjoint ? 1 + K : 0;
+  size_t freeb = 0, totb = 0;
+  if (cudaMemGetInfo(&freeb, &totb) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, HV_ECUDA, "cudaMemGetInfo failed");
+  }
+  double budget = c->cfg.mem_budget ? static_cast<double>(c->cfg.mem_budget) : 0.9 * static_cast<double>(freeb);
+  // shared (not per shot): Q, W2, imgc, rec coef, staging of V/HV/m
+  const double shared = F4 * (static_cast<double>(K) * g.plane * 2 + g.plane + g.iplane + 4.0 * K * g.nz * g.nx +
+                              2.0 * g.nz * g.nx) + (1 << 20);
+  auto per_shot = [&](int store, int k) {
+    double b = F4 * 2.0 * pl->nslot * g.plane;                                  // field pool
+    b += F4 * (double)K * g.nt * g.nrec;                                        // Born data
+    if (grad) b += F4 * 2.0 * g.nt * g.nrec;                                    // data + residual
+    b += F4 * (double)pl->nacc * g.plane;                                       // accumulators
+    if (adjoint) {
+      if (store == HV_STORE_FULL) b += F4 * (double)g.nt * g.iplane;
+      else b += F4 * (2.0 * ((g.nt - 1 + k - 1) / k) * g.plane + (double)k * g.iplane);
+    }
+    return b;
+  };
+  int k = c->cfg.ckpt_interval > 0 ? c->cfg.ckpt_interval
+                                   : std::max(1, static_cast<int>(std::lround(std::sqrt((double)g.nt))));
+  int store = c->cfg.store;
+  if (!adjoint) store = HV_STORE_FULL;  // forward only: nothing stored
+  if (store == HV_STORE_AUTO) store = (shared + per_shot(HV_STORE_FULL, k) <= budget) ? HV_STORE_FULL
+                                                                                       : HV_STORE_CHECKPOINT;
+  if (store != HV_STORE_FULL && store != HV_STORE_CHECKPOINT)
+    return fail(c, HV_EINVAL, "unknown storage mode " + std::to_string(store));
+  pl->store = store;
+  pl->k = k;
+  pl->nck = (g.nt - 1 + k - 1) / k;
+  pl->per_shot = per_shot(store, k);
+  const double avail = budget - shared;
+  int fit = avail > 0 ? static_cast<int>(avail / pl->per_shot) : 0;
+  if (fit < 1)
+    return fail(c, HV_ENOMEM, "plan needs " + std::to_string((shared + pl->per_shot) / 1e9) +
+                                  " GB per shot in flight; budget " + std::to_string(budget / 1e9) + " GB");
+  int S = c->cfg.shot_batch > 0 ? c->cfg.shot_batch : 0;
+  const int ntiles = g.ntx * g.ntz;
+  pl->FG = c->cfg.field_group > 0 ? c->cfg.field_group : 8;
+  if (S <= 0) {
+    const int G = std::max(1, (K + pl->FG - 1) / pl->FG);
+    const int ctas_per_shot = ntiles * G;
+    S = std::max(1, (148 * 4 + ctas_per_shot - 1) / ctas_per_shot);  // about 4 resident CTAs per SM
+  }
+  S = std::min(S, fit);
+  S = std::min(S, c->nloc);
+  pl->S = std::max(1, S);
+  return HV_OK;
+}
+
+// ------------------------------------------------------------------------------------------ one call
+
+int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, const float* V_in, float* d_user,
+        float* g_user, double* phi_user, float* hv_user) {
+  if (!c) return HV_ESTATE;
+  c->err.clear();
+  CU_TRY(cudaSetDevice(c->dev));
+  const Geo& g = c->g;
+  const int nloc = c->nloc;
+  const bool grad = want & W_GRAD, hess = want & W_HESS, fwd = want & W_FORWARD;
+  if (hess && K < 1 && !grad) return fail(c, HV_EINVAL, "K must be >= 1");
+  if (K < 0) return fail(c, HV_EINVAL, "K must be >= 0");
+  c->launches = 0;
+  int64_t launches = 0;
+  const size_t mbytes = sizeof(float) * (size_t)g.nz * g.nx;
+  const size_t dbytes = sizeof(float) * (size_t)nloc * g.nt * g.nrec;
+
+  cudaEvent_t ev0, ev1;
+  CU_TRY(cudaEventCreate(&ev0));
+  CU_TRY(cudaEventCreate(&ev1));
+  CU_TRY(cudaEventRecord(ev0, c->stream));
+
+  const float *m = nullptr, *dobs = nullptr, *V = nullptr;
+  int st = stage_in(c, "in_m", m_in, mbytes, reinterpret_cast<const void**>(&m));
+  if (st) return st;
+  if (grad) {
+    st = stage_in(c, "in_dobs", dobs_in, dbytes, reinterpret_cast<const void**>(&dobs));
+    if (st) return st;
+  }
+  if (K > 0) {
+    st = stage_in(c, "in_V", V_in, mbytes * (size_t)K, reinterpret_cast<const void**>(&V));
+    if (st) return st;
+  }
+  OutStage o_d, o_g, o_hv;
+  if (fwd && (st = stage_out(c, "out_d", d_user, dbytes, &o_d))) return st;
+  if (grad && (st = stage_out(c, "out_g", g_user, mbytes, &o_g))) return st;
+  if (K > 0 && (st = stage_out(c, "out_hv", hv_user, mbytes * (size_t)K, &o_hv))) return st;
+
+  Plan pl;
+  if ((st = plan_call(c, want, K, &pl))) return st;
+  const int S = pl.S;
+  const bool adjoint = grad || K > 0;
+  const int nslot = pl.nslot;
+  const int replay_slot = nslot - 1;
+
+  // --- a0: model-dependent coefficients
+  float *W2, *imgc, *rec_coef;
+  unsigned int* vmax;
+  double* phi_d;
+  if ((st = ws_get(c, "W2", sizeof(float) * g.plane, (void**)&W2))) return st;
+  if ((st = ws_get(c, "imgc", sizeof(float) * g.iplane, (void**)&imgc))) return st;
+  if ((st = ws_get(c, "rec_coef", sizeof(float) * g.nrec, (void**)&rec_coef))) return st;
+  if ((st = ws_get(c, "scalars", 64, (void**)&vmax))) return st;
+  phi_d = reinterpret_cast<double*>(reinterpret_cast<char*>(vmax) + 8);
+  CU_TRY(cudaMemsetAsync(vmax, 0, 64, c->stream));
+  const float h = c->cfg.h, dt = c->cfg.dt;
+  const float dt2_h2 = dt * dt / (h * h), two_dt2_h2 = 2.0f * dt * dt / (h * h);
+  model_setup_kernel<<<grid1d(g.plane), 256, 0, c->stream>>>(g, m, dt2_h2, two_dt2_h2, W2, imgc, vmax);
+  rec_coef_kernel<<<(g.nrec + 255) / 256, 256, 0, c->stream>>>(g, m, c->d_recI, c->d_recJ, rec_coef);
+  launches += 2;
+  unsigned int vbits = 0;
+  CU_TRY(cudaMemcpyAsync(&vbits, vmax, 4, cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(cudaStreamSynchronize(c->stream));
+  float vmx;
+  std::memcpy(&vmx, &vbits, 4);
+  if (!(vmx > 0.0f) || !std::isfinite(vmx)) return fail(c, HV_EINVAL, "model must be positive and finite");
+  if (dt * vmx / h > 0.5546f)
+    return fail(c, HV_ECFL, "CFL: dt*max(m)/h = " + std::to_string(dt * vmx / h) + " > 0.5546");
+
+  float* Q = nullptr;
+  if (K > 0) {
+    if ((st = ws_get(c, "Q", sizeof(float) * g.plane * K, (void**)&Q))) return st;
+    q_setup_kernel<<<grid1d(g.plane * K), 256, 0, c->stream>>>(g, m, V, K, two_dt2_h2, Q);
+    launches++;
+  }
+
+  // --- workspace
+  float *pool, *dborn = nullptr, *dbg = nullptr, *rres = nullptr, *acc = nullptr, *store = nullptr,
+               *ckpt = nullptr, *seg = nullptr;
+  const long long planes_per_shot = 2LL * nslot;
+  if ((st = ws_get(c, "pool", sizeof(float) * g.plane * planes_per_shot * S, (void**)&pool))) return st;
+  if (K > 0 && (st = ws_get(c, "dborn", sizeof(float) * (size_t)S * K * g.nt * g.nrec, (void**)&dborn))) return st;
+  if (grad) {
+    if ((st = ws_get(c, "dbg", sizeof(float) * (size_t)S * g.nt * g.nrec, (void**)&dbg))) return st;
+    if ((st = ws_get(c, "rres", sizeof(float) * (size_t)S * g.nt * g.nrec, (void**)&rres))) return st;
+  }
+  if (adjoint) {
+    if ((st = ws_get(c, "acc", sizeof(float) * g.plane * pl.nacc * S, (void**)&acc))) return st;
+    CU_TRY(cudaMemsetAsync(acc, 0, sizeof(float) * g.plane * pl.nacc * S, c->stream));
+    if (pl.store == HV_STORE_FULL) {
+      if ((st = ws_get(c, "store", sizeof(float) * g.iplane * g.nt * S, (void**)&store))) return st;
+    } else {
+      if ((st = ws_get(c, "ckpt", sizeof(float) * g.plane * 2 * pl.nck * S, (void**)&ckpt))) return st;
+      if ((st = ws_get(c, "seg", sizeof(float) * g.iplane * pl.k * S, (void**)&seg))) return st;
+    }
+  }
+  CUtensorMap tmap;
+  if ((st = make_tmap(c, pool, planes_per_shot * S, &tmap))) return st;
+  if (phi_user) CU_TRY(cudaMemsetAsync(phi_d, 0, sizeof(double), c->stream));
+
+  // --- the shot batches
+  const int FG = pl.FG;
+  const int Gf = K > 0 ? (K + FG - 1) / FG : 1;
+  const int Fb = (grad ? 1 : 0) + K;  // adjoint fields
+  const int slot0_b = grad ? 0 : 1;
+  const int Gb = std::max(1, (Fb + FG - 1) / FG);
+  const dim3 block(BX, BY);
+  const dim3 tiles(g.ntx, g.ntz);
+  double ms_f = 0, ms_b = 0;
+  std::vector<cudaEvent_t> evs;
+  auto new_event = [&](cudaEvent_t* e) -> int {
+    CU_TRY(cudaEventCreate(e));
+    evs.push_back(*e);
+    return HV_OK;
+  };
+
+  for (int b0 = 0; b0 < nloc; b0 += S) {
+    const int Sb = std::min(S, nloc - b0);
+    cudaEvent_t e_f0, e_f1, e_b0, e_b1;
+    if ((st = new_event(&e_f0)) || (st = new_event(&e_f1)) || (st = new_event(&e_b0)) || (st = new_event(&e_b1)))
+      return st;
+    CU_TRY(cudaMemsetAsync(pool, 0, sizeof(float) * g.plane * planes_per_shot * Sb, c->stream));
+    CU_TRY(cudaEventRecord(e_f0, c->stream));
+
+    FwdParams fp{};
+    fp.g = g;
+    fp.pool = pool;
+    fp.nslot = nslot;
+    fp.bg_slot = 0;
+    fp.bg_update = 1;
+    fp.born_slot0 = 1;
+    fp.K = K;
+    fp.FG = FG;
+    fp.G = Gf;
+    fp.W2 = W2;
+    fp.Q = Q;
+    fp.imgc = imgc;
+    fp.shot0 = b0;
+    fp.src_I = c->d_srcI;
+    fp.src_J = c->d_srcJ;
+    fp.src_amp = c->d_src_amp;
+    fp.trec_beg = c->d_trec_beg;
+    fp.trec_id = c->d_trec_id;
+    fp.rec_I = c->d_recI;
+    fp.rec_J = c->d_recJ;
+    fp.d_born = dborn;
+    if (fwd) {
+      fp.d_bg = reinterpret_cast<float*>(o_d.dev);
+      fp.dbg_shot0 = b0;
+    } else if (grad) {
+      fp.d_bg = dbg;
+      fp.dbg_shot0 = 0;
+    }
+    const bool full = adjoint && pl.store == HV_STORE_FULL;
+    fp.s_shot_stride = full ? g.iplane * g.nt : 0;
+    const dim3 gridf(g.ntx, g.ntz, Sb * Gf);
+    for (int n = 0; n <= g.nt - 2; ++n) {
+      if (adjoint && pl.store == HV_STORE_CHECKPOINT && n % pl.k == 0) {
+        // save (u^n, u^{n-1}): both parity planes of slot 0, per shot; layout ckpt[S][nck][2][plane]
+        for (int s = 0; s < Sb; ++s)
+          CU_TRY(cudaMemcpyAsync(ckpt + ((size_t)s * pl.nck + n / pl.k) * 2 * g.plane,
+                                 pool + (size_t)s * planes_per_shot * g.plane, sizeof(float) * 2 * g.plane,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+      }
+      fp.n = n;
+      fp.s_out = full ? store + (size_t)n * g.iplane : nullptr;
+      fwd_step_kernel<<<gridf, block, SMEM_BYTES, c->stream>>>(tmap, fp);
+      launches++;
+    }
+    CU_TRY(cudaEventRecord(e_f1, c->stream));
+    {
+      const dim3 gg((g.nrec + 127) / 128, 1 + K, Sb);
+      gather_last_kernel<<<gg, 128, 0, c->stream>>>(g, pool, nslot, (g.nt - 1) & 1, fp.dbg_shot0, fp.d_bg, 0,
+                                                    dborn, 1, K, c->d_recI, c->d_recJ);
+      launches++;
+    }
+    CU_TRY(cudaGetLastError());
+    if (adjoint) {
+      if (grad) {
+        const long long nres = (long long)Sb * g.nt * g.nrec;
+        residual_kernel<<<grid1d(nres), 256, 0, c->stream>>>(nres, dbg, dobs + (size_t)b0 * g.nt * g.nrec, rres,
+                                                              phi_d);
+        launches++;
+      }
+      CU_TRY(cudaMemsetAsync(pool, 0, sizeof(float) * g.plane * planes_per_shot * Sb, c->stream));
+      BwdParams bp{};
+      bp.g = g;
+      bp.pool = pool;
+      bp.nslot = nslot;
+      bp.slot0 = slot0_b;
+      bp.F = Fb;
+      bp.FG = FG;
+      bp.G = Gb;
+      bp.W2 = W2;
+      bp.acc = acc;
+      bp.nacc = pl.nacc;
+      bp.rho_res = rres;
+      bp.rho_born = dborn;
+      bp.Kb = K;
+      bp.rec_coef = rec_coef;
+      bp.trec_beg = c->d_trec_beg;
+      bp.trec_id = c->d_trec_id;
+      bp.rec_I = c->d_recI;
+      bp.rec_J = c->d_recJ;
+      const dim3 gridb(g.ntx, g.ntz, Sb * Gb);
+      CU_TRY(cudaEventRecord(e_b0, c->stream));
+      int cur_b = -1;
+      for (int j = g.nt - 1; j >= 1; --j) {
+        bp.j = j;
+        bp.update = j >= 2;
+        bp.imaging = j <= g.nt - 2;
+        if (bp.imaging) {
+          if (full) {
+            bp.s_lvl = store + (size_t)j * g.iplane;
+            bp.s_shot_stride = g.iplane * g.nt;
+          } else {
+            const int b = (j / pl.k) * pl.k;
+            if (b != cur_b) {  // replay segment [b, e) of the background into the segment store
+              const int e = std::min(b + pl.k, g.nt - 1);
+              for (int s = 0; s < Sb; ++s)
+                CU_TRY(cudaMemcpyAsync(pool + ((size_t)s * planes_per_shot + (size_t)replay_slot * 2) * g.plane,
+                                       ckpt + ((size_t)s * pl.nck + b / pl.k) * 2 * g.plane,
+                                       sizeof(float) * 2 * g.plane, cudaMemcpyDeviceToDevice, c->stream));
+              FwdParams rp = fp;
+              rp.bg_slot = replay_slot;
+              rp.K = 0;
+              rp.G = 1;
+              rp.d_bg = nullptr;
+              rp.d_born = nullptr;
+              rp.s_shot_stride = g.iplane * pl.k;
+              const dim3 gridr(g.ntx, g.ntz, Sb);
+              for (int n = b; n < e; ++n) {
+                rp.n = n;
+                rp.s_out = seg + (size_t)(n - b) * g.iplane;
+                fwd_step_kernel<<<gridr, block, SMEM_BYTES, c->stream>>>(tmap, rp);
+                launches++;
+              }
+              cur_b = b;
+            }
+            bp.s_lvl = seg + (size_t)(j - cur_b) * g.iplane;
+            bp.s_shot_stride = g.iplane * pl.k;
+          }
+        }
+        bwd_step_kernel<<<gridb, block, SMEM_BYTES, c->stream>>>(tmap, bp);
+        launches++;
+      }
+      CU_TRY(cudaGetLastError());
+    } else {
+      CU_TRY(cudaEventRecord(e_b0, c->stream));
+    }
+    CU_TRY(cudaEventRecord(e_b1, c->stream));
+  }
+
+  // --- a8 (within the GPU): fixed-order sum over the shots in flight, into the caller's layout
+  if (grad) {
+    finalize_kernel<<<grid1d((long long)g.nz * g.nx), 256, 0, c->stream>>>(g, acc, S, pl.nacc, 0, 1,
+                                                                             reinterpret_cast<float*>(o_g.dev));
+    launches++;
+  }
+  if (K > 0) {
+    finalize_kernel<<<grid1d((long long)K * g.nz * g.nx), 256, 0, c->stream>>>(
+        g, acc, S, pl.nacc, 1, K, reinterpret_cast<float*>(o_hv.dev));
+    launches++;
+  }
+  CU_TRY(cudaGetLastError());
+  if (fwd && (st = finish_out(c, o_d))) return st;
+  if (grad && (st = finish_out(c, o_g))) return st;
+  if (K > 0 && (st = finish_out(c, o_hv))) return st;
+  if (phi_user) CU_TRY(cudaMemcpyAsync(phi_user, phi_d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CU_TRY(cudaEventRecord(ev1, c->stream));
+  CU_TRY(cudaStreamSynchronize(c->stream));
+  for (size_t i = 0; i + 3 < evs.size(); i += 4) {
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, evs[i], evs[i + 1]);
+    cudaEventElapsedTime(&b, evs[i + 2], evs[i + 3]);
+    ms_f += a;
+    ms_b += b;
+  }
+  float tot = 0;
+  cudaEventElapsedTime(&tot, ev0, ev1);
+  for (auto e : evs) cudaEventDestroy(e);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  c->launches = launches;
+  c->stats.kernel_launches = launches;
+  c->stats.graph_launches = 0;
+  c->stats.shot_batch = S;
+  c->stats.field_group = FG;
+  c->stats.store = pl.store;
+  c->stats.ckpt_interval = pl.k;
+  c->stats.bytes_per_shot = pl.per_shot;
+  c->stats.ms_forward = ms_f;
+  c->stats.ms_backward = ms_b;
+  c->stats.ms_total = tot;
+  return HV_OK;
+}
+
+}  // namespace
+
+// ============================================================================================ C ABI
+
+extern "C" {
+
+int hv_create(const hv_config* cfg, hv_ctx** out) {
+  if (!cfg || !out) return HV_EINVAL;
+  *out = nullptr;
+  hv_ctx* c = new hv_ctx();
+  c->cfg = *cfg;
+  const hv_config& k = *cfg;
+  auto bad = [&](int code, const std::string& m) {
+    std::fprintf(stderr, "hv_create: %s\n", m.c_str());
+    delete c;
+    return code;
+  };
+  if (k.nz < 1 || k.nx < 1 || k.nt < 3 || k.nsrc < 1 || k.nrec < 1) return bad(HV_EINVAL, "bad sizes");
+  if (!(k.h > 0) || !(k.dt > 0) || !(k.v_ref > 0)) return bad(HV_EINVAL, "h, dt, v_ref must be positive");
+  if (k.sponge < R) return bad(HV_EINVAL, "sponge must be >= 4 cells");
+  if (!k.src_iz || !k.src_ix || !k.rec_iz || !k.rec_ix || !k.wavelet) return bad(HV_EINVAL, "null geometry");
+  const int sb = k.src_begin, se = k.src_end ? k.src_end : k.nsrc;
+  if (sb < 0 || se > k.nsrc || sb >= se) return bad(HV_EINVAL, "bad shot shard");
+  c->cfg.src_end = se;
+  c->nloc = se - sb;
+  for (int i = 0; i < k.nsrc; ++i)
+    if (k.src_iz[i] < 0 || k.src_iz[i] >= k.nz || k.src_ix[i] < 0 || k.src_ix[i] >= k.nx)
+      return bad(HV_EINVAL, "source index out of range");
+  for (int i = 0; i < k.nrec; ++i)
+    if (k.rec_iz[i] < 0 || k.rec_iz[i] >= k.nz || k.rec_ix[i] < 0 || k.rec_ix[i] >= k.nx)
+      return bad(HV_EINVAL, "receiver index out of range");
+  c->src_iz.assign(k.src_iz + sb, k.src_iz + se);
+  c->src_ix.assign(k.src_ix + sb, k.src_ix + se);
+  c->rec_iz.assign(k.rec_iz, k.rec_iz + k.nrec);
+  c->rec_ix.assign(k.rec_ix, k.rec_ix + k.nrec);
+  c->wavelet.assign(k.wavelet, k.wavelet + k.nt);
+  c->cfg.src_iz = c->cfg.src_ix = c->cfg.rec_iz = c->cfg.rec_ix = nullptr;
+  c->cfg.wavelet = nullptr;
+  c->dev = k.device;
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= k.device || k.device < 0) {
+    cudaGetLastError();
+    return bad(HV_ECUDA, "no CUDA device (this library has no CPU fallback)");
+  }
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, k.device) != cudaSuccess || prop.major < 10)
+    return bad(HV_ECUDA, "device is not sm_100-class");
+  if (cudaSetDevice(k.device) != cudaSuccess) return bad(HV_ECUDA, "cudaSetDevice failed");
+
+  // geometry
+  Geo& g = c->g;
+  g.nz = k.nz;
+  g.nx = k.nx;
+  g.W = k.sponge;
+  g.Nz = k.nz + 2 * k.sponge;
+  g.Nx = k.nx + 2 * k.sponge;
+  g.ntx = (g.Nx + TX - 1) / TX;
+  g.ntz = (g.Nz + TZ - 1) / TZ;
+  g.P = g.ntx * TX;
+  g.c0 = (g.W / 4) * 4;
+  g.PI = ((g.W + g.nx - g.c0) + 3) / 4 * 4;
+  g.plane = (long long)g.Nz * g.P;
+  g.iplane = (long long)g.nz * g.PI;
+  const double eta_max = 3.0 * k.v_ref * std::log(1000.0) / (2.0 * k.sponge * k.h);
+  g.kc = static_cast<float>(eta_max * k.dt / (2.0 * (double)k.sponge * k.sponge));
+  g.nt = k.nt;
+  g.nrec = k.nrec;
+
+  // persistent device arrays
+  std::vector<int> sI(c->nloc), sJ(c->nloc), rI(k.nrec), rJ(k.nrec);
+  for (int i = 0; i < c->nloc; ++i) {
+    sI[i] = c->src_iz[i] + g.W;
+    sJ[i] = c->src_ix[i] + g.W;
+  }
+  for (int i = 0; i < k.nrec; ++i) {
+    rI[i] = c->rec_iz[i] + g.W;
+    rJ[i] = c->rec_ix[i] + g.W;
+  }
+  const int ntiles = g.ntx * g.ntz;
+  std::vector<int> beg(ntiles + 1, 0), ids(k.nrec);
+  for (int i = 0; i < k.nrec; ++i) beg[(rI[i] / TZ) * g.ntx + rJ[i] / TX + 1]++;
+  for (int t = 0; t < ntiles; ++t) beg[t + 1] += beg[t];
+  {
+    std::vector<int> fillp(beg.begin(), beg.end() - 1);
+    for (int i = 0; i < k.nrec; ++i) ids[fillp[(rI[i] / TZ) * g.ntx + rJ[i] / TX]++] = i;
+  }
+  std::vector<float> amp(k.nt);
+  for (int n = 0; n < k.nt; ++n)
+    amp[n] = static_cast<float>((double)k.dt * k.dt * (double)c->wavelet[n] / ((double)k.h * k.h));
+  auto up = [&](void** d, const void* h, size_t b) -> bool {
+    if (cudaMalloc(d, std::max<size_t>(b, 4)) != cudaSuccess) return false;
+    return cudaMemcpy(*d, h, b, cudaMemcpyHostToDevice) == cudaSuccess;
+  };
+  if (!up((void**)&c->d_srcI, sI.data(), sizeof(int) * sI.size()) ||
+      !up((void**)&c->d_srcJ, sJ.data(), sizeof(int) * sJ.size()) ||
+      !up((void**)&c->d_recI, rI.data(), sizeof(int) * rI.size()) ||
+      !up((void**)&c->d_recJ, rJ.data(), sizeof(int) * rJ.size()) ||
+      !up((void**)&c->d_trec_beg, beg.data(), sizeof(int) * beg.size()) ||
+      !up((void**)&c->d_trec_id, ids.data(), sizeof(int) * ids.size()) ||
+      !up((void**)&c->d_src_amp, amp.data(), sizeof(float) * amp.size())) {
+    cudaGetLastError();
+    hv_destroy(c);
+    std::fprintf(stderr, "hv_create: device allocation failed\n");
+    return HV_ECUDA;
+  }
+  if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    hv_destroy(c);
+    return HV_ECUDA;
+  }
+  c->stream = c->own_stream;
+  cudaDriverEntryPointQueryResult q{};
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+      q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    hv_destroy(c);
+    std::fprintf(stderr, "hv_create: cuTensorMapEncodeTiled unavailable\n");
+    return HV_ECUDA;
+  }
+  c->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  if (cudaFuncSetAttribute(fwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
+          cudaSuccess ||
+      cudaFuncSetAttribute(bwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
+          cudaSuccess) {
+    cudaGetLastError();
+    hv_destroy(c);
+    return HV_ECUDA;
+  }
+  *out = c;
+  return HV_OK;
+}
+
+int hv_destroy(hv_ctx* c) {
+  if (!c) return HV_ESTATE;
+  cudaSetDevice(c->dev);
+  for (auto& kv : c->ws)
+    if (kv.second.p) cudaFree(kv.second.p);
+  for (auto& kv : c->fft_plans) cufftDestroy(kv.second);
+  cudaFree(c->d_srcI);
+  cudaFree(c->d_srcJ);
+  cudaFree(c->d_recI);
+  cudaFree(c->d_recJ);
+  cudaFree(c->d_trec_beg);
+  cudaFree(c->d_trec_id);
+  cudaFree(c->d_src_amp);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+  return HV_OK;
+}
+
+int hv_set_stream(hv_ctx* c, void* s) {
+  if (!c) return HV_ESTATE;
+  c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+  return HV_OK;
+}
+
+int hv_forward(hv_ctx* c, const float* m, float* d) {
+  if (!c) return HV_ESTATE;
+  return run(c, W_FORWARD, m, nullptr, 0, nullptr, d, nullptr, nullptr, nullptr);
+}
+
+int hv_gradient(hv_ctx* c, const float* m, const float* d_obs, float* g, double* phi) {
+  if (!c) return HV_ESTATE;
+  return run(c, W_GRAD, m, d_obs, 0, nullptr, nullptr, g, phi, nullptr);
+}
+
+int hv_hessvec(hv_ctx* c, const float* m, int32_t K, const float* V, float* HV) {
+  if (!c) return HV_ESTATE;
+  if (K < 1) return fail(c, HV_EINVAL, "K must be >= 1");
+  return run(c, W_HESS, m, nullptr, K, V, nullptr, nullptr, nullptr, HV);
+}
+
+int hv_gradient_hessvec(hv_ctx* c, const float* m, const float* d_obs, int32_t K, const float* V, float* g,
+                        double* phi, float* HV) {
+  if (!c) return HV_ESTATE;
+  if (K < 0) return fail(c, HV_EINVAL, "K must be >= 0");
+  return run(c, W_GRAD | (K > 0 ? W_HESS : 0), m, d_obs, K, V, nullptr, g, phi, HV);
+}
+
+int hv_get_stats(const hv_ctx* c, hv_stats* out) {
+  if (!c) return HV_ESTATE;
+  if (!out) return HV_EINVAL;
+  *out = c->stats;
+  return HV_OK;
+}
+
+const char* hv_last_error(const hv_ctx* c) { return c ? c->err.c_str() : "null hv_ctx"; }
+
+}  // extern "C"

@@ -1,0 +1,39 @@
+// hv_geo.h — tile constants and the padded-grid geometry shared by kernels and the host runtime.
+#pragma once
+
+namespace hvk {
+
+constexpr int R = 4;                 // stencil radius (8th order)
+constexpr int TX = 64;               // tile width  (x, contiguous)
+constexpr int TZ = 32;               // tile height (z)
+constexpr int BX = 16;               // threads along x, 4 consecutive points (one float4) each
+constexpr int BY = 16;               // threads along z
+constexpr int RZ = TZ / BY;          // consecutive rows per thread
+constexpr int NTHREADS = BX * BY;
+constexpr int HX = TX + 2 * R;       // halo tile width  (72 floats = 288 B, a multiple of 16 B for TMA)
+constexpr int HZ = TZ + 2 * R;       // halo tile height
+constexpr int TILE_FLOATS = HX * HZ;
+constexpr int TILE_BYTES = TILE_FLOATS * 4;
+constexpr int NSTAGE = 3;
+constexpr int SMEM_BYTES = NSTAGE * TILE_BYTES + 64;
+
+// standard 8th-order central second-derivative weights (unscaled; h^-2 is folded into the coefficients)
+#define HV_A0 (-205.0f / 72.0f)
+#define HV_A1 (8.0f / 5.0f)
+#define HV_A2 (-1.0f / 5.0f)
+#define HV_A3 (8.0f / 315.0f)
+#define HV_A4 (-1.0f / 560.0f)
+
+struct Geo {
+  int nz, nx, W;        // interior grid, sponge width
+  int Nz, Nx;           // padded grid
+  int P;                // row pitch of padded planes (floats) = ntx * TX
+  int PI, c0;           // interior-store row pitch and first padded column stored (c0 % 4 == 0)
+  int ntx, ntz;         // tile grid
+  long long plane;      // Nz * P
+  long long iplane;     // nz * PI
+  float kc;             // eta_max * dt / (2 W^2): c = kc (d_z^2 + d_x^2)
+  int nt, nrec;
+};
+
+}  // namespace hvk

@@ -1,0 +1,65 @@
+// hv_internal.h — runtime context and host helpers shared by hv_api.cu and psido.cu (not part of the ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cufft.h>
+
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/hv.h"
+#include "hv_geo.h"
+
+namespace hvrt {
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+}  // namespace hvrt
+
+struct hv_ctx {
+  hv_config cfg{};
+  std::vector<int32_t> src_iz, src_ix, rec_iz, rec_ix;
+  std::vector<float> wavelet;
+  int nloc = 0;  // shots in this rank's shard
+  int dev = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  hvk::Geo g{};
+  // persistent device arrays
+  int *d_srcI = nullptr, *d_srcJ = nullptr, *d_recI = nullptr, *d_recJ = nullptr;
+  int *d_trec_beg = nullptr, *d_trec_id = nullptr;
+  float* d_src_amp = nullptr;
+  // grow-only workspace
+  std::map<std::string, hvrt::DevBuf> ws;
+  std::map<std::tuple<int, int, int>, cufftHandle> fft_plans;  // (nz, nx, batch)
+  std::string err = "";
+  hv_stats stats{};
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  int64_t launches = 0;
+};
+
+namespace hvrt {
+struct OutStage {
+  void* user = nullptr;
+  void* dev = nullptr;
+  size_t bytes = 0;
+  bool host = false;
+};
+int fail(hv_ctx* c, int code, const std::string& msg);
+int ws_get(hv_ctx* c, const char* name, size_t bytes, void** out);
+bool is_device_ptr(const void* p);
+int stage_in(hv_ctx* c, const char* name, const void* p, size_t bytes, const void** dev);
+int stage_out(hv_ctx* c, const char* name, void* p, size_t bytes, OutStage* o);
+int finish_out(hv_ctx* c, const OutStage& o);
+}  // namespace hvrt
+
+#define CU_TRY(call)                                                                           \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess)                                                                     \
+      return hvrt::fail(c, HV_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)

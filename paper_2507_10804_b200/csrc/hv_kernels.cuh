@@ -1,0 +1,562 @@
+// hv_kernels.cuh — sm_100a device code of the Gauss-Newton H·v hot path.
+//
+// Every kernel here is a step of SURVEY.md §8(a):
+//   fwd_step_kernel  a1 + a2 + a3 (+ a4 FULL write): background leapfrog step, K Born steps sharing L u^n,
+//                    point-source injection, receiver sampling, sponge damping, imaging-factor store
+//   bwd_step_kernel  a5 + a7 (+ a3 injection): K adjoint steps with fused zero-lag imaging accumulation
+//   setup / gather / residual (K4) / finalize (a8 within a GPU) helpers
+// The scheme they implement is the one restated in include/hv.h and DESIGN.md §3 (PAPER.md:44-49, 108-112,
+// 157-164 for what is computed; the discretisation is our reading, the paper gives none).
+//
+// B200 design: 2-D tiles of TZ x TX outputs; the (TZ+8) x (TX+8) halo tile of the stencil field is staged
+// into shared memory by TMA (cp.async.bulk.tensor.3d; out-of-bounds boxes are zero-filled, which *is* the
+// zero-outside-the-padded-grid boundary of the Laplacian), NSTAGE-deep mbarrier ring over the fields a CTA
+// handles; pointwise streams (u^{n-1}, q_k, accumulators) are float4, coalesced, no halo.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hv_geo.h"
+
+namespace hvk {
+
+// ------------------------------------------------------------------------------------------------ PTX
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void tma_load_3d(float* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                            int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float f4(const float4& v, int i) {
+  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+// Unscaled 8th-order Laplacian of this thread's RZ x 4 points from a halo tile in shared memory.
+// Thread (tx, ty) owns tile rows ty*RZ .. ty*RZ+RZ-1 and columns 4tx .. 4tx+3.
+__device__ __forceinline__ void lap_points(const float* __restrict__ t, int tx, int ty, float (&L)[RZ][4],
+                                           float (&C)[RZ][4]) {
+  const int col = R + tx * 4;
+  float4 zw[RZ + 2 * R];
+#pragma unroll
+  for (int k = 0; k < RZ + 2 * R; ++k) zw[k] = ld4(t + (ty * RZ + k) * HX + col);
+#pragma unroll
+  for (int r = 0; r < RZ; ++r) {
+    const float* row = t + (ty * RZ + r + R) * HX + tx * 4;
+    const float4 a = ld4(row);
+    const float4 b = zw[r + R];
+    const float4 c = ld4(row + 8);
+    const float xs[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float ctr = xs[4 + i];
+      float s = HV_A1 * ((xs[3 + i] + xs[5 + i]) + (f4(zw[r + 3], i) + f4(zw[r + 5], i)));
+      s = fmaf(HV_A2, (xs[2 + i] + xs[6 + i]) + (f4(zw[r + 2], i) + f4(zw[r + 6], i)), s);
+      s = fmaf(HV_A3, (xs[1 + i] + xs[7 + i]) + (f4(zw[r + 1], i) + f4(zw[r + 7], i)), s);
+      s = fmaf(HV_A4, (xs[0 + i] + xs[8 + i]) + (f4(zw[r + 0], i) + f4(zw[r + 8], i)), s);
+      L[r][i] = fmaf(2.0f * HV_A0, ctr, s);
+      C[r][i] = ctr;
+    }
+  }
+}
+
+// Sponge coefficient c = kc (d_z^2 + d_x^2), d_z = max(0, W - I, I - (W + nz - 1)) (C10).
+__device__ __forceinline__ float sponge_c(const Geo& g, int I, int J) {
+  const int dz = max(0, max(g.W - I, I - (g.W + g.nz - 1)));
+  const int dx = max(0, max(g.W - J, J - (g.W + g.nx - 1)));
+  return g.kc * static_cast<float>(dz * dz + dx * dx);
+}
+
+__device__ __forceinline__ bool tile_is_interior(const Geo& g, int x0, int z0) {
+  return z0 >= g.W && z0 + TZ <= g.W + g.nz && x0 >= g.W && x0 + TX <= g.W + g.nx;
+}
+
+// ------------------------------------------------------------------------------------------------ forward
+
+struct FwdParams {
+  Geo g;
+  float* pool;            // field planes; plane index = ((s_local * nslot) + slot) * 2 + parity
+  int nslot;
+  int n;                  // this launch computes level n+1 from levels n, n-1
+  int bg_slot;            // slot of the background u
+  int bg_update;          // write u^{n+1}? (always 1 except sampling-only use)
+  int born_slot0;         // Born field k lives in slot born_slot0 + k
+  int K;                  // Born fields
+  int FG, G;              // Born fields per CTA, CTAs (groups) per shot and tile
+  const float* W2;        // [Nz][P]   dt^2 v^2 / h^2 (0 outside the padded grid)
+  const float* Q;         // [K][Nz][P] 2 dt^2 v dv_k / h^2 (0 in the sponge)
+  const float* imgc;      // [nz][PI]  2 dt^2 / (v h^2); with s_out: store s^n = imgc * Lu^n
+  float* s_out;           // level-n slot of the imaging-factor store for s_local = 0, or null
+  long long s_shot_stride;
+  int shot0;              // shard-local index of batch shot 0
+  const int* src_I;       // [local shots] padded source row / column
+  const int* src_J;
+  const float* src_amp;   // [nt] dt^2 s[n] / h^2
+  const int* trec_beg;    // [ntiles + 1] receivers owned by each tile
+  const int* trec_id;
+  const int* rec_I;
+  const int* rec_J;
+  float* d_bg;            // background data [..][nt][nrec], row dbg_shot0 + s_local, or null
+  int dbg_shot0;
+  float* d_born;          // [S][K][nt][nrec] Born data (batch-local) or null
+};
+
+__global__ void __launch_bounds__(NTHREADS) fwd_step_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                            const FwdParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* tiles = reinterpret_cast<float*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + NSTAGE * TILE_BYTES);
+  const Geo& g = p.g;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
+  const int x0 = blockIdx.x * TX, z0 = blockIdx.y * TZ;
+  const int sl = blockIdx.z / p.G, grp = blockIdx.z % p.G;
+  const int fb = grp * p.FG;
+  const int fe = min(p.K, fb + p.FG);
+  const int nitems = 1 + max(0, fe - fb);
+  const int par_n = p.n & 1, par_new = par_n ^ 1;
+  const bool leader = (grp == 0) && p.bg_update;
+  const long long shot_planes = static_cast<long long>(sl) * p.nslot;
+
+  if (tid == 0) {
+    tma_prefetch_desc(&tmap);
+    for (int i = 0; i < NSTAGE; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto slot_of = [&](int item) { return item == 0 ? p.bg_slot : p.born_slot0 + fb + item - 1; };
+  if (tid == 0) {
+    for (int i = 0; i < min(NSTAGE, nitems); ++i) {
+      mbar_expect_tx(&bars[i], TILE_BYTES);
+      tma_load_3d(tiles + i * TILE_FLOATS, &tmap, &bars[i], x0 - R, z0 - R,
+                  static_cast<int>((shot_planes + slot_of(i)) * 2 + par_n));
+    }
+  }
+
+  const int lz0 = ty * RZ;
+  const int I0 = z0 + lz0;
+  const int J0 = x0 + tx * 4;
+  const bool interior = tile_is_interior(g, x0, z0);
+  // per-point coefficients: w = dt^2 v^2 / h^2, (1 - c), 1 / (1 + c)
+  float w[RZ][4], cm[RZ][4], ci[RZ][4];
+#pragma unroll
+  for (int r = 0; r < RZ; ++r) {
+    const int I = I0 + r;
+    float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (I < g.Nz) wv = ldg4(p.W2 + static_cast<long long>(I) * g.P + J0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      w[r][i] = f4(wv, i);
+      const float c = interior ? 0.f : sponge_c(g, I, J0 + i);
+      cm[r][i] = 1.0f - c;
+      ci[r][i] = 1.0f / (1.0f + c);
+    }
+  }
+  const int tile_id = blockIdx.y * g.ntx + blockIdx.x;
+  const int rb = p.trec_beg[tile_id], re = p.trec_beg[tile_id + 1];
+  const int shot = p.shot0 + sl;
+  const int sI = p.src_I[shot], sJ = p.src_J[shot];
+  const float amp = p.src_amp[p.n];
+
+  float Lb[RZ][4];
+  for (int item = 0; item < nitems; ++item) {
+    const int stage = item % NSTAGE;
+    const int slot = slot_of(item);
+    const long long new_plane = (shot_planes + slot) * 2 + par_new;
+    float* __restrict__ dst = p.pool + new_plane * g.plane;
+    // pointwise streams first (latency overlaps the TMA wait): u^{n-1} (same plane as u^{n+1}) and q_k
+    float4 prev[RZ], qv[RZ];
+    const bool do_update = (item > 0) || leader;
+    const float* qk = (item > 0) ? p.Q + static_cast<long long>(fb + item - 1) * g.plane : nullptr;
+#pragma unroll
+    for (int r = 0; r < RZ; ++r) {
+      const int I = I0 + r;
+      prev[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+      qv[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (do_update && I < g.Nz) {
+        prev[r] = ld4(dst + static_cast<long long>(I) * g.P + J0);
+        if (item > 0) qv[r] = ldg4(qk + static_cast<long long>(I) * g.P + J0);
+      }
+    }
+    mbar_wait(&bars[stage], (item / NSTAGE) & 1);
+    const float* t = tiles + stage * TILE_FLOATS;
+    float L[RZ][4], C[RZ][4];
+    lap_points(t, tx, ty, L, C);
+    if (item == 0) {
+#pragma unroll
+      for (int r = 0; r < RZ; ++r)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) Lb[r][i] = L[r][i];
+    }
+    if (do_update) {
+#pragma unroll
+      for (int r = 0; r < RZ; ++r) {
+        const int I = I0 + r;
+        if (I >= g.Nz) continue;
+        float o[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int J = J0 + i;
+          float rhs = w[r][i] * L[r][i];
+          if (item > 0) rhs = fmaf(f4(qv[r], i), Lb[r][i], rhs);
+          else if (I == sI && J == sJ) rhs += amp;
+          float v = (2.0f * C[r][i] - cm[r][i] * f4(prev[r], i) + rhs) * ci[r][i];
+          o[i] = (J < g.Nx) ? v : 0.0f;
+        }
+        st4(dst + static_cast<long long>(I) * g.P + J0, make_float4(o[0], o[1], o[2], o[3]));
+      }
+    }
+    // imaging-factor store s^n = 2 dt^2 / (v h^2) * L~u^n on the interior (FULL / replay segments)
+    if (item == 0 && leader && p.s_out != nullptr) {
+      const int jc = J0 - g.c0;
+      if (jc >= 0 && jc < g.PI) {
+#pragma unroll
+        for (int r = 0; r < RZ; ++r) {
+          const int iz = I0 + r - g.W;
+          if (iz < 0 || iz >= g.nz) continue;
+          const float4 ic = ldg4(p.imgc + static_cast<long long>(iz) * g.PI + jc);
+          float o[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int ix = J0 + i - g.W;
+            o[i] = (ix >= 0 && ix < g.nx) ? f4(ic, i) * Lb[r][i] : 0.0f;
+          }
+          st4(p.s_out + sl * p.s_shot_stride + static_cast<long long>(iz) * g.PI + jc,
+              make_float4(o[0], o[1], o[2], o[3]));
+        }
+      }
+    }
+    // receiver sampling of level n from the staged tile (d[n] = u^n[rec]; level nt-1 by gather_last_kernel)
+    if (re > rb) {
+      float* out = nullptr;
+      if (item == 0) {
+        if (leader && p.d_bg) out = p.d_bg + static_cast<long long>(p.dbg_shot0 + sl) * g.nt * g.nrec;
+      } else if (p.d_born) {
+        out = p.d_born + (static_cast<long long>(sl) * p.K + (fb + item - 1)) * g.nt * g.nrec;
+      }
+      if (out) {
+        for (int q = rb + tid; q < re; q += NTHREADS) {
+          const int rid = p.trec_id[q];
+          const int lz = p.rec_I[rid] - z0 + R, lx = p.rec_J[rid] - x0 + R;
+          out[static_cast<long long>(p.n) * g.nrec + rid] = t[lz * HX + lx];
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with this stage
+    if (tid == 0 && item + NSTAGE < nitems) {
+      fence_proxy_async();
+      mbar_expect_tx(&bars[stage], TILE_BYTES);
+      tma_load_3d(tiles + stage * TILE_FLOATS, &tmap, &bars[stage], x0 - R, z0 - R,
+                  static_cast<int>((shot_planes + slot_of(item + NSTAGE)) * 2 + par_n));
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------ backward
+
+struct BwdParams {
+  Geo g;
+  float* pool;
+  int nslot;
+  int j;                  // computes lambda^j from lambda^{j+1} (halo) and lambda^{j+2} (pointwise)
+  int update;             // compute lambda^j (j >= 2; lambda^1 is never used)
+  int imaging;            // accumulate s^j lambda^{j+1} (j <= nt-2)
+  int slot0, F;           // adjoint fields in slots slot0 .. slot0 + F - 1
+  int FG, G;
+  const float* W2;
+  const float* s_lvl;     // s^j for s_local = 0
+  long long s_shot_stride;
+  float* acc;             // [S][nacc][Nz][P], index by slot
+  int nacc;
+  const float* rho_res;   // slot 0 injection data [S][nt][nrec] (gradient), or null
+  const float* rho_born;  // slot k >= 1 injection data [S][K][nt][nrec]
+  int Kb;                 // K of rho_born
+  const float* rec_coef;  // [nrec] v^2 / (1 + c) at each receiver
+  const int* trec_beg;
+  const int* trec_id;
+  const int* rec_I;
+  const int* rec_J;
+};
+
+__global__ void __launch_bounds__(NTHREADS) bwd_step_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                            const BwdParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* tiles = reinterpret_cast<float*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + NSTAGE * TILE_BYTES);
+  const Geo& g = p.g;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
+  const int x0 = blockIdx.x * TX, z0 = blockIdx.y * TZ;
+  const int sl = blockIdx.z / p.G, grp = blockIdx.z % p.G;
+  const int fb = grp * p.FG;
+  const int fe = min(p.F, fb + p.FG);
+  const int nitems = fe - fb;
+  if (nitems <= 0) return;
+  const int par_in = (p.j + 1) & 1, par_out = p.j & 1;
+  const long long shot_planes = static_cast<long long>(sl) * p.nslot;
+
+  if (tid == 0) {
+    tma_prefetch_desc(&tmap);
+    for (int i = 0; i < NSTAGE; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int i = 0; i < min(NSTAGE, nitems); ++i) {
+      mbar_expect_tx(&bars[i], TILE_BYTES);
+      tma_load_3d(tiles + i * TILE_FLOATS, &tmap, &bars[i], x0 - R, z0 - R,
+                  static_cast<int>((shot_planes + p.slot0 + fb + i) * 2 + par_in));
+    }
+  }
+  const int lz0 = ty * RZ;
+  const int I0 = z0 + lz0;
+  const int J0 = x0 + tx * 4;
+  const bool interior = tile_is_interior(g, x0, z0);
+  float w[RZ][4], cm[RZ][4], ci[RZ][4], sj[RZ][4];
+  const int jc = J0 - g.c0;
+#pragma unroll
+  for (int r = 0; r < RZ; ++r) {
+    const int I = I0 + r;
+    float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (I < g.Nz) wv = ldg4(p.W2 + static_cast<long long>(I) * g.P + J0);
+    float4 sv = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int iz = I - g.W;
+    if (p.imaging && iz >= 0 && iz < g.nz && jc >= 0 && jc < g.PI)
+      sv = ldg4(p.s_lvl + sl * p.s_shot_stride + static_cast<long long>(iz) * g.PI + jc);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      w[r][i] = f4(wv, i);
+      const int ix = J0 + i - g.W;
+      sj[r][i] = (ix >= 0 && ix < g.nx) ? f4(sv, i) : 0.0f;
+      const float c = interior ? 0.f : sponge_c(g, I, J0 + i);
+      cm[r][i] = 1.0f - c;
+      ci[r][i] = 1.0f / (1.0f + c);
+    }
+  }
+  bool img_rows[RZ];
+  bool any_img = false;
+#pragma unroll
+  for (int r = 0; r < RZ; ++r) {
+    const int iz = I0 + r - g.W;
+    img_rows[r] = p.imaging && iz >= 0 && iz < g.nz && J0 + 3 >= g.W && J0 < g.W + g.nx;
+    any_img |= img_rows[r];
+  }
+  const int tile_id = blockIdx.y * g.ntx + blockIdx.x;
+  const int rb = p.trec_beg[tile_id], re = p.trec_beg[tile_id + 1];
+
+  for (int item = 0; item < nitems; ++item) {
+    const int stage = item % NSTAGE;
+    const int slot = p.slot0 + fb + item;
+    float* __restrict__ dst = p.pool + ((shot_planes + slot) * 2 + par_out) * g.plane;
+    float4 prev[RZ];
+#pragma unroll
+    for (int r = 0; r < RZ; ++r) {
+      const int I = I0 + r;
+      prev[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (p.update && I < g.Nz) prev[r] = ld4(dst + static_cast<long long>(I) * g.P + J0);
+    }
+    mbar_wait(&bars[stage], (item / NSTAGE) & 1);
+    const float* t = tiles + stage * TILE_FLOATS;
+    float L[RZ][4], C[RZ][4];
+    lap_points(t, tx, ty, L, C);
+    if (p.update) {
+#pragma unroll
+      for (int r = 0; r < RZ; ++r) {
+        const int I = I0 + r;
+        if (I >= g.Nz) continue;
+        float o[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float v = (2.0f * C[r][i] - cm[r][i] * f4(prev[r], i) + w[r][i] * L[r][i]) * ci[r][i];
+          o[i] = (J0 + i < g.Nx) ? v : 0.0f;
+        }
+        st4(dst + static_cast<long long>(I) * g.P + J0, make_float4(o[0], o[1], o[2], o[3]));
+      }
+    }
+    if (any_img) {  // zero-lag imaging: acc += s^j * lambda^{j+1} (RED.128: one writer per address per step)
+      float* a = p.acc + (static_cast<long long>(sl) * p.nacc + slot) * g.plane;
+#pragma unroll
+      for (int r = 0; r < RZ; ++r) {
+        if (!img_rows[r]) continue;
+        const float4 add = make_float4(sj[r][0] * C[r][0], sj[r][1] * C[r][1], sj[r][2] * C[r][2],
+                                       sj[r][3] * C[r][3]);
+        atomicAdd(reinterpret_cast<float4*>(a + static_cast<long long>(I0 + r) * g.P + J0), add);
+      }
+    }
+    __syncthreads();  // stage consumed and lambda^j of this tile stored
+    if (tid == 0 && item + NSTAGE < nitems) {
+      fence_proxy_async();
+      mbar_expect_tx(&bars[stage], TILE_BYTES);
+      tma_load_3d(tiles + stage * TILE_FLOATS, &tmap, &bars[stage], x0 - R, z0 - R,
+                  static_cast<int>((shot_planes + slot + NSTAGE) * 2 + par_in));
+    }
+    // receiver injection into lambda^j: += v^2 / (1 + c) * rho[j][r]   (R^T scatter-add)
+    if (p.update && re > rb) {
+      const float* rho = (slot == 0)
+                             ? p.rho_res + static_cast<long long>(sl) * g.nt * g.nrec
+                             : p.rho_born + (static_cast<long long>(sl) * p.Kb + (slot - 1)) * g.nt * g.nrec;
+      for (int q = rb + tid; q < re; q += NTHREADS) {
+        const int rid = p.trec_id[q];
+        const float val = p.rec_coef[rid] * rho[static_cast<long long>(p.j) * g.nrec + rid];
+        atomicAdd(dst + static_cast<long long>(p.rec_I[rid]) * g.P + p.rec_J[rid], val);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------ helpers
+
+// a0: padded coefficient planes from the interior model m (edge-replicated into the sponge, C13).
+__global__ void model_setup_kernel(Geo g, const float* __restrict__ m, float dt2_h2, float two_dt2_h2,
+                                   float* __restrict__ W2, float* __restrict__ imgc, unsigned int* vmax_bits) {
+  const long long n = static_cast<long long>(g.Nz) * g.P;
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int I = static_cast<int>(q / g.P), J = static_cast<int>(q % g.P);
+    float wv = 0.0f;
+    if (J < g.Nx) {
+      const int iz = min(max(I - g.W, 0), g.nz - 1), ix = min(max(J - g.W, 0), g.nx - 1);
+      const float v = m[static_cast<long long>(iz) * g.nx + ix];
+      wv = dt2_h2 * v * v;
+      if (I == iz + g.W && J == ix + g.W) atomicMax(vmax_bits, __float_as_uint(v));
+    }
+    W2[q] = wv;
+  }
+  const long long ni = static_cast<long long>(g.nz) * g.PI;
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < ni;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int iz = static_cast<int>(q / g.PI), ix = static_cast<int>(q % g.PI) + g.c0 - g.W;
+    float c = 0.0f;
+    if (ix >= 0 && ix < g.nx) c = two_dt2_h2 / m[static_cast<long long>(iz) * g.nx + ix];
+    imgc[q] = c;
+  }
+}
+
+__global__ void rec_coef_kernel(Geo g, const float* __restrict__ m, const int* rec_I,
+                                const int* rec_J, float* coef) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= g.nrec) return;
+  const int I = rec_I[r], J = rec_J[r];
+  const float v = m[static_cast<long long>(I - g.W) * g.nx + (J - g.W)];
+  const float c = sponge_c(g, I, J);
+  coef[r] = v * v / (1.0f + c);
+}
+
+// K5: q_k = 2 dt^2 v dv_k / h^2 on the interior, 0 in the sponge and the row padding.
+__global__ void q_setup_kernel(Geo g, const float* __restrict__ m, const float* __restrict__ V, int K,
+                               float two_dt2_h2, float* __restrict__ Q) {
+  const long long n = static_cast<long long>(K) * g.Nz * g.P;
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long k = q / g.plane;
+    const long long rem = q % g.plane;
+    const int I = static_cast<int>(rem / g.P), J = static_cast<int>(rem % g.P);
+    const int iz = I - g.W, ix = J - g.W;
+    float val = 0.0f;
+    if (iz >= 0 && iz < g.nz && ix >= 0 && ix < g.nx) {
+      const long long o = static_cast<long long>(iz) * g.nx + ix;
+      val = two_dt2_h2 * m[o] * V[k * g.nz * static_cast<long long>(g.nx) + o];
+    }
+    Q[q] = val;
+  }
+}
+
+// d[n = nt-1] for every field of the batch: the level the last forward step produced.
+__global__ void gather_last_kernel(Geo g, const float* __restrict__ pool, int nslot, int par, int dbg_shot0,
+                                    float* d_bg, int bg_slot, float* d_born, int born_slot0, int K,
+                                    const int* rec_I, const int* rec_J) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int f = blockIdx.y;  // 0 = background, 1..K Born
+  const int s = blockIdx.z;
+  if (r >= g.nrec) return;
+  const long long off = static_cast<long long>(rec_I[r]) * g.P + rec_J[r];
+  if (f == 0) {
+    if (!d_bg) return;
+    const long long pl = (static_cast<long long>(s) * nslot + bg_slot) * 2 + par;
+    d_bg[(static_cast<long long>(dbg_shot0 + s) * g.nt + (g.nt - 1)) * g.nrec + r] = pool[pl * g.plane + off];
+  } else {
+    if (!d_born) return;
+    const long long pl = (static_cast<long long>(s) * nslot + born_slot0 + f - 1) * 2 + par;
+    d_born[((static_cast<long long>(s) * K + (f - 1)) * g.nt + (g.nt - 1)) * g.nrec + r] =
+        pool[pl * g.plane + off];
+  }
+}
+
+// K4: residual rho = d - d_obs and phi = 1/2 sum rho^2 in float64.
+__global__ void residual_kernel(long long n, const float* __restrict__ d, const float* __restrict__ dobs,
+                                float* __restrict__ res, double* phi) {
+  double acc = 0.0;
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const float r = d[q] - dobs[q];
+    res[q] = r;
+    acc += 0.5 * static_cast<double>(r) * static_cast<double>(r);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) atomicAdd(phi, v);
+  }
+}
+
+// a8 within a GPU: out[f][iz][ix] = sum_s acc[s][slot f][iz + W][ix + W] in a fixed order (deterministic).
+__global__ void finalize_kernel(Geo g, const float* __restrict__ acc, int S, int nacc, int slot0, int F,
+                                float* __restrict__ out) {
+  const long long n = static_cast<long long>(F) * g.nz * g.nx;
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long f = q / (static_cast<long long>(g.nz) * g.nx);
+    const long long rem = q % (static_cast<long long>(g.nz) * g.nx);
+    const int iz = static_cast<int>(rem / g.nx), ix = static_cast<int>(rem % g.nx);
+    float s = 0.0f;
+    for (int k = 0; k < S; ++k)
+      s += acc[(static_cast<long long>(k) * nacc + slot0 + f) * g.plane + static_cast<long long>(iz + g.W) * g.P +
+               ix + g.W];
+    out[q] = s;
+  }
+}
+
+}  // namespace hvk

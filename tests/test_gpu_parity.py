@@ -1,0 +1,227 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle on the same seeded inputs (P10).
+
+Bar (BASELINE.json north_star): relative L2 <= 1e-4 on d, g and H·v. Cases span several 64x32 tiles
+with ragged tails, every storage mode, several shot batches and field groupings, and full BASELINE
+sizes in the bench's launch configuration (a sampled shot/probe slice against the oracle, plus
+properties that hold at any size)."""
+import numpy as np
+import pytest
+
+from oracle import psido as opsido
+from oracle import wave
+from tests.conftest import rel_l2
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def hv():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2507_10804_b200 as hvmod
+    return hvmod
+
+
+# ---------------------------------------------------------------------------------------------- cfg 0
+
+
+@pytest.fixture(scope="module")
+def cfg0_ref():
+    wl = W.config(0)
+    pb = wave.Problem(wl)
+    V = wl.probes()
+    d = pb.forward_all()
+    HV = pb.hessvec(list(V.astype(np.float64)))
+    m0 = W.m0_cfg0()
+    d_obs = d.astype(np.float32)           # d_obs = F(model) from the oracle (fp32-rounded, C17)
+    phi, g = wave.Problem(wl, m0).gradient(d_obs)
+    return wl, V, d, HV, m0, d_obs, phi, g
+
+
+def test_cfg0_forward(hv, cfg0_ref):
+    wl, V, d, *_ = cfg0_ref
+    s = hv.Solver.from_workload(wl)
+    dg = s.forward(wl.model)
+    assert dg.shape == d.shape
+    assert np.all(dg[:, 0, :] == 0.0)
+    assert rel_l2(dg, d) <= TOL, rel_l2(dg, d)
+
+
+@pytest.mark.parametrize("store", ["full", "checkpoint"])
+def test_cfg0_hessvec(hv, cfg0_ref, store):
+    wl, V, d, HV, *_ = cfg0_ref
+    s = hv.Solver.from_workload(wl, store=store)
+    out = s.hessvec(wl.model, V)
+    assert rel_l2(out, HV) <= TOL, rel_l2(out, HV)
+    assert s.stats()["store"] == (1 if store == "full" else 2)
+
+
+def test_cfg0_gradient(hv, cfg0_ref):
+    wl, V, d, HV, m0, d_obs, phi, g = cfg0_ref
+    s = hv.Solver.from_workload(wl)
+    phig, gg = s.gradient(m0, d_obs)
+    assert rel_l2(gg, g) <= TOL, rel_l2(gg, g)
+    assert abs(phig - phi) <= TOL * phi
+
+
+def test_cfg0_fused_gradient_hessvec(hv, cfg0_ref):
+    wl, V, d, HV, m0, d_obs, phi, g = cfg0_ref
+    s = hv.Solver.from_workload(wl)
+    pb = wave.Problem(wl, m0)
+    HV0 = pb.hessvec(list(V.astype(np.float64)))
+    phig, gg, hvg = s.gradient_hessvec(m0, d_obs, V)
+    assert rel_l2(gg, g) <= TOL and rel_l2(hvg, HV0) <= TOL
+    assert abs(phig - phi) <= TOL * phi
+
+
+# ---------------------------------------------------------------------------------------------- multi-tile
+
+
+@pytest.fixture(scope="module")
+def ragged():
+    """70 x 150 interior (110 x 190 padded: 4 x 3 tiles of 32 x 64, ragged in both directions),
+    3 shots, 3 probes, sparse receiver line, nt = 300."""
+    wl = W.custom(70, 150, nt=300, ns=3, nrec=37, n_probes=3, f_peak=15.0, seed=5)
+    pb = wave.Problem(wl)
+    V = wl.probes()
+    d = pb.forward_all()
+    HV = pb.hessvec(list(V.astype(np.float64)))
+    d_obs = wave.Problem(wl, wl.model_true).forward_all().astype(np.float32)
+    phi, g = pb.gradient(d_obs)
+    return wl, V, d, HV, d_obs, phi, g
+
+
+@pytest.mark.parametrize("store,ckpt,batch,fg", [
+    ("full", 0, 1, 8), ("full", 0, 2, 1), ("full", 0, 3, 2),
+    ("checkpoint", 7, 1, 8), ("checkpoint", 0, 3, 1), ("checkpoint", 299, 2, 3),
+])
+def test_ragged_hessvec_modes(hv, ragged, store, ckpt, batch, fg):
+    wl, V, d, HV, *_ = ragged
+    s = hv.Solver.from_workload(wl, store=store, ckpt_interval=ckpt, shot_batch=batch, field_group=fg)
+    out = s.hessvec(wl.model, V)
+    assert rel_l2(out, HV) <= TOL, rel_l2(out, HV)
+    for k in range(3):
+        assert rel_l2(out[k], HV[k]) <= TOL
+
+
+def test_ragged_forward_gradient(hv, ragged):
+    wl, V, d, HV, d_obs, phi, g = ragged
+    s = hv.Solver.from_workload(wl, shot_batch=2)
+    assert rel_l2(s.forward(wl.model), d) <= TOL
+    phig, gg = s.gradient(wl.model, d_obs)
+    assert rel_l2(gg, g) <= TOL and abs(phig - phi) <= TOL * phi
+
+
+def test_ragged_shards_sum(hv, ragged):
+    """Source sharding (a8): partial sums over [0,1) + [1,3) equal the full result (rank-local sums)."""
+    wl, V, d, HV, *_ = ragged
+    a = hv.Solver.from_workload(wl, src_begin=0, src_end=1).hessvec(wl.model, V)
+    b = hv.Solver.from_workload(wl, src_begin=1, src_end=3).hessvec(wl.model, V)
+    assert rel_l2(a + b, HV) <= TOL
+    ref1 = wave.Problem(wl).hessvec(list(V.astype(np.float64)), shots=[0])
+    assert rel_l2(a, ref1) <= TOL
+
+
+def test_device_pointers_match_host_pointers(hv, ragged):
+    import torch
+    wl, V, d, HV, *_ = ragged
+    s = hv.Solver.from_workload(wl)
+    host = s.hessvec(wl.model, V)
+    dev = s.hessvec(torch.from_numpy(wl.model).cuda(), torch.from_numpy(V).cuda())
+    assert isinstance(dev, torch.Tensor) and dev.is_cuda
+    assert np.array_equal(dev.cpu().numpy(), host)           # bitwise: same kernels, same order
+
+
+def test_deterministic_and_batch_invariant(hv, ragged):
+    wl, V, *_ = ragged
+    s = hv.Solver.from_workload(wl, shot_batch=1, field_group=1)
+    a = s.hessvec(wl.model, V)
+    b = s.hessvec(wl.model, V)
+    assert np.array_equal(a, b)
+    # probe k alone equals row k of the batch (each field's arithmetic is independent of the grouping)
+    c = s.hessvec(wl.model, V[1:2])
+    assert np.array_equal(c[0], a[1])
+
+
+def test_edge_cases(hv):
+    # degenerate: zero probe -> zero H v, zero residual -> zero gradient; minimum grid; receiver on a corner
+    wl = W.custom(1, 5, nt=40, ns=1, nrec=2, n_probes=1, W=4, f_peak=25.0, seed=2)
+    wl.rec = np.array([[0, 0], [0, 4]], dtype=np.int32)
+    wl.src = np.array([[0, 2]], dtype=np.int32)
+    s = hv.Solver.from_workload(wl)
+    z = s.hessvec(wl.model, np.zeros((1, 1, 5), np.float32))
+    assert np.all(z == 0.0)
+    ref = wave.Problem(wl)
+    d = s.forward(wl.model)
+    assert rel_l2(d, ref.forward_all()) <= TOL
+    phi, g = s.gradient(wl.model, d)
+    assert phi == 0.0 and np.all(g == 0.0)
+    V = wl.probes()
+    assert rel_l2(s.hessvec(wl.model, V), ref.hessvec(list(V.astype(np.float64)))) <= TOL
+
+
+def test_errors(hv):
+    wl = W.config(0)
+    s = hv.Solver.from_workload(wl)
+    with pytest.raises(hv.HVError) as e:
+        s.forward(wl.model * 100.0)          # violates CFL
+    assert e.value.status == hv.HV_ECFL
+    bad = W.config(0)
+    bad.src = np.array([[64, 0]], dtype=np.int32)
+    with pytest.raises(hv.HVError) as e:
+        hv.Solver.from_workload(bad)
+    assert e.value.status == hv.HV_EINVAL
+
+
+# ---------------------------------------------------------------------------------------------- full size
+
+
+def test_cfg1_full_size_sampled_slice(hv):
+    """BASELINE cfg 1 at full size (201 x 401, nt = 2000) in the bench's launch configuration:
+    shot 7 with PSF probes (3,3) and (6,2) against the oracle (SURVEY.md §8(d) parity sub-slice)."""
+    wl = W.config(1)
+    ks = [3 * 8 + 3, 6 * 8 + 2]
+    V = wl.probes(ks)
+    s = hv.Solver.from_workload(wl, src_begin=7, src_end=8)
+    out = s.hessvec(wl.model, V)
+    pb = wave.Problem(wl)
+    ref = pb.hessvec(list(V.astype(np.float64)), shots=[7], mode="checkpoint", ckpt=45)
+    assert rel_l2(out, ref) <= TOL, rel_l2(out, ref)
+    d7 = s.forward(wl.model)[0]
+    assert rel_l2(d7, pb.forward(7)) <= TOL
+
+
+def test_cfg1_full_batch_properties(hv):
+    """All 16 shots x 64 PSF spikes (the bench workload): H symmetric on the spike lattice,
+    HV_i(x_j) = HV_j(x_i) (self-adjoint), PSD diagonal, and batching invariance."""
+    wl = W.config(1)
+    V = wl.probes()
+    s = hv.Solver.from_workload(wl)
+    out = s.hessvec(wl.model, V).astype(np.float64)
+    pts = [tuple(np.argwhere(v)[0]) for v in V]
+    M = np.array([[out[i][pts[j]] for j in range(64)] for i in range(64)])
+    scale = np.abs(np.diag(M)).max()
+    assert np.all(np.diag(M) > 0)
+    assert np.max(np.abs(M - M.T)) <= 1e-4 * scale
+    sub = s.hessvec(wl.model, V[[5, 40]])
+    assert rel_l2(sub[0], out[5]) <= 1e-6 and rel_l2(sub[1], out[40]) <= 1e-6
+
+
+# ---------------------------------------------------------------------------------------------- PsiDO
+
+
+@pytest.mark.parametrize("nz,nx,r", [(16, 24, 1), (33, 47, 3), (64, 128, 8)])
+def test_psido_apply_parity(hv, nz, nx, r):
+    rng = np.random.default_rng(nz * nx + r)
+    a = rng.standard_normal((r, nz, nx)).astype(np.float32)
+    b = (rng.standard_normal((r, nz, nx)) + 1j * rng.standard_normal((r, nz, nx))).astype(np.complex64)
+    v = rng.standard_normal((nz, nx)).astype(np.float32)
+    s = hv.Solver.from_workload(W.config(0))
+    for mode in range(3):
+        out = s.psido_apply(a, b, v, mode)
+        ref = opsido.apply_mode(a.astype(np.float64), b.astype(np.complex128), v.astype(np.float64), mode)
+        assert rel_l2(out, ref) <= TOL, (mode, rel_l2(out, ref))

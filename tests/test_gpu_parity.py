@@ -36,8 +36,10 @@ def cfg0_ref():
     V = wl.probes()
     d = pb.forward_all()
     HV = pb.hessvec(list(V.astype(np.float64)))
-    m0 = W.m0_cfg0()
-    d_obs = d.astype(np.float32)           # d_obs = F(model) from the oracle (fp32-rounded, C17)
+    # gradient recipe (DESIGN.md §3 R-grad): d_obs = F(model) from the oracle (fp32-rounded, C17), evaluated at
+    # a 4 % slow starting model, so the residual is O(|d|) and fp32 rounding of d is not amplified
+    m0 = (0.96 * W.m0_cfg0()).astype(np.float32)
+    d_obs = d.astype(np.float32)
     phi, g = wave.Problem(wl, m0).gradient(d_obs)
     return wl, V, d, HV, m0, d_obs, phi, g
 
@@ -68,6 +70,23 @@ def test_cfg0_gradient(hv, cfg0_ref):
     assert abs(phig - phi) <= TOL * phi
 
 
+def test_cfg0_gradient_near_zero_residual(hv, cfg0_ref):
+    """The SURVEY.md §8(d) recipe (m0 = anomaly removed) leaves a residual of only 0.28 % of |d|, so the fp32
+    rounding of the forward data (eps_d <= 1e-5 relative) is amplified by |d| / |rho| in
+    rho = d - d_obs. Derived bound: rel_l2(g) <= 1e-4 + 2 eps_d |d| / |rho|."""
+    wl, V, d, HV, m0, d_obs, phi, g = cfg0_ref
+    m1 = W.m0_cfg0()
+    pb = wave.Problem(wl, m1)
+    phi1, g1 = pb.gradient(d_obs)
+    rho = pb.forward_all() - d_obs
+    ratio = np.linalg.norm(d_obs) / np.linalg.norm(rho)
+    s = hv.Solver.from_workload(wl)
+    phig, gg = s.gradient(m1, d_obs)
+    tol = 1e-4 + 2 * 1e-5 * ratio
+    assert rel_l2(gg, g1) <= tol, (rel_l2(gg, g1), tol)
+    assert abs(phig - phi1) <= tol * phi1
+
+
 def test_cfg0_fused_gradient_hessvec(hv, cfg0_ref):
     wl, V, d, HV, m0, d_obs, phi, g = cfg0_ref
     s = hv.Solver.from_workload(wl)
@@ -91,8 +110,9 @@ def ragged():
     d = pb.forward_all()
     HV = pb.hessvec(list(V.astype(np.float64)))
     d_obs = wave.Problem(wl, wl.model_true).forward_all().astype(np.float32)
-    phi, g = pb.gradient(d_obs)
-    return wl, V, d, HV, d_obs, phi, g
+    m_start = (0.96 * wl.model).astype(np.float32)          # well-conditioned residual (R-grad)
+    phi, g = wave.Problem(wl, m_start).gradient(d_obs)
+    return wl, V, d, HV, d_obs, phi, g, m_start
 
 
 @pytest.mark.parametrize("store,ckpt,batch,fg", [
@@ -109,10 +129,10 @@ def test_ragged_hessvec_modes(hv, ragged, store, ckpt, batch, fg):
 
 
 def test_ragged_forward_gradient(hv, ragged):
-    wl, V, d, HV, d_obs, phi, g = ragged
+    wl, V, d, HV, d_obs, phi, g, m_start = ragged
     s = hv.Solver.from_workload(wl, shot_batch=2)
     assert rel_l2(s.forward(wl.model), d) <= TOL
-    phig, gg = s.gradient(wl.model, d_obs)
+    phig, gg = s.gradient(m_start, d_obs)
     assert rel_l2(gg, g) <= TOL and abs(phig - phi) <= TOL * phi
 
 
@@ -200,15 +220,15 @@ def test_cfg1_full_batch_properties(hv):
     HV_i(x_j) = HV_j(x_i) (self-adjoint), PSD diagonal, and batching invariance."""
     wl = W.config(1)
     V = wl.probes()
-    s = hv.Solver.from_workload(wl)
+    s = hv.Solver.from_workload(wl, shot_batch=2)
     out = s.hessvec(wl.model, V).astype(np.float64)
     pts = [tuple(np.argwhere(v)[0]) for v in V]
     M = np.array([[out[i][pts[j]] for j in range(64)] for i in range(64)])
     scale = np.abs(np.diag(M)).max()
     assert np.all(np.diag(M) > 0)
     assert np.max(np.abs(M - M.T)) <= 1e-4 * scale
-    sub = s.hessvec(wl.model, V[[5, 40]])
-    assert rel_l2(sub[0], out[5]) <= 1e-6 and rel_l2(sub[1], out[40]) <= 1e-6
+    sub = s.hessvec(wl.model, V[[5, 40]])            # same shot batching -> bitwise identical rows
+    assert np.array_equal(sub[0], out[5].astype(np.float32)) and np.array_equal(sub[1], out[40].astype(np.float32))
 
 
 # ---------------------------------------------------------------------------------------------- PsiDO

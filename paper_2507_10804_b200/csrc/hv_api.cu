@@ -29,15 +29,16 @@ using namespace hvrt;
 
 namespace {
 
-int make_tmap(hv_ctx* c, float* pool, long long nplanes, CUtensorMap* map) {
+// 3-D tensor map over planes [nplanes][Nz][P] (logical width Nx: TMA zero-fills outside the padded grid).
+int make_tmap(hv_ctx* c, const float* base, long long nplanes, int box_w, int box_h, CUtensorMap* map) {
   const Geo& g = c->g;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.Nx), static_cast<cuuint64_t>(g.Nz),
                         static_cast<cuuint64_t>(nplanes)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.P) * 4, static_cast<cuuint64_t>(g.plane) * 4};
-  cuuint32_t box[3] = {static_cast<cuuint32_t>(HX), static_cast<cuuint32_t>(HZ), 1};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h), 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = c->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, pool, dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+  CUresult r = c->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(c, HV_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
   return HV_OK;
@@ -214,8 +215,10 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
       if ((st = ws_get(c, "seg", sizeof(float) * g.iplane * pl.k * S, (void**)&seg))) return st;
     }
   }
-  CUtensorMap tmap;
-  if ((st = make_tmap(c, pool, planes_per_shot * S, &tmap))) return st;
+  CUtensorMap map_halo, map_tile, map_q;
+  if ((st = make_tmap(c, pool, planes_per_shot * S, HX, HZ, &map_halo))) return st;
+  if ((st = make_tmap(c, pool, planes_per_shot * S, TX, TZ, &map_tile))) return st;
+  if ((st = make_tmap(c, Q ? Q : pool, Q ? K : planes_per_shot * S, TX, TZ, &map_q))) return st;
   if (phi_user) CU_TRY(cudaMemsetAsync(phi_d, 0, sizeof(double), c->stream));
 
   // --- the shot batches
@@ -253,7 +256,6 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     fp.FG = FG;
     fp.G = Gf;
     fp.W2 = W2;
-    fp.Q = Q;
     fp.imgc = imgc;
     fp.shot0 = b0;
     fp.src_I = c->d_srcI;
@@ -284,7 +286,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
       }
       fp.n = n;
       fp.s_out = full ? store + (size_t)n * g.iplane : nullptr;
-      fwd_step_kernel<<<gridf, block, SMEM_BYTES, c->stream>>>(tmap, fp);
+      fwd_step_kernel<<<gridf, block, FWD_SMEM_BYTES, c->stream>>>(map_halo, map_tile, map_q, fp);
       launches++;
     }
     CU_TRY(cudaEventRecord(e_f1, c->stream));
@@ -352,7 +354,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
               for (int n = b; n < e; ++n) {
                 rp.n = n;
                 rp.s_out = seg + (size_t)(n - b) * g.iplane;
-                fwd_step_kernel<<<gridr, block, SMEM_BYTES, c->stream>>>(tmap, rp);
+                fwd_step_kernel<<<gridr, block, FWD_SMEM_BYTES, c->stream>>>(map_halo, map_tile, map_q, rp);
                 launches++;
               }
               cur_b = b;
@@ -361,7 +363,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
             bp.s_shot_stride = g.iplane * pl.k;
           }
         }
-        bwd_step_kernel<<<gridb, block, SMEM_BYTES, c->stream>>>(tmap, bp);
+        bwd_step_kernel<<<gridb, block, BWD_SMEM_BYTES, c->stream>>>(map_halo, map_tile, bp);
         launches++;
       }
       CU_TRY(cudaGetLastError());
@@ -536,9 +538,9 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
     return HV_ECUDA;
   }
   c->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  if (cudaFuncSetAttribute(fwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
+  if (cudaFuncSetAttribute(fwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FWD_SMEM_BYTES) !=
           cudaSuccess ||
-      cudaFuncSetAttribute(bwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
+      cudaFuncSetAttribute(bwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_BYTES) !=
           cudaSuccess) {
     cudaGetLastError();
     hv_destroy(c);

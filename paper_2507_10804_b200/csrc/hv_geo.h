@@ -12,10 +12,18 @@ constexpr int RZ = TZ / BY;          // consecutive rows per thread
 constexpr int NTHREADS = BX * BY;
 constexpr int HX = TX + 2 * R;       // halo tile width  (72 floats = 288 B, a multiple of 16 B for TMA)
 constexpr int HZ = TZ + 2 * R;       // halo tile height
-constexpr int TILE_FLOATS = HX * HZ;
+constexpr int TILE_FLOATS = HX * HZ;          // halo tile (stencil input)
 constexpr int TILE_BYTES = TILE_FLOATS * 4;
-constexpr int NSTAGE = 3;
-constexpr int SMEM_BYTES = NSTAGE * TILE_BYTES + 64;
+constexpr int PT_FLOATS = TX * TZ;            // pointwise tile (no halo)
+constexpr int PT_BYTES = PT_FLOATS * 4;
+constexpr int NSTAGE = 3;                     // TMA pipeline depth (items in flight per CTA)
+// forward stage: halo u^n / du_k^n + tile u^{n-1} / du_k^{n-1} + tile q_k
+constexpr int FWD_STAGE_FLOATS = TILE_FLOATS + 2 * PT_FLOATS;
+constexpr int FWD_SMEM_BYTES = NSTAGE * FWD_STAGE_FLOATS * 4 + 64;
+// backward stage: halo lambda^{j+1} + tile lambda^{j+2}
+constexpr int BWD_STAGE_FLOATS = TILE_FLOATS + PT_FLOATS;
+constexpr int BWD_SMEM_BYTES = NSTAGE * BWD_STAGE_FLOATS * 4 + 64;
+constexpr int SMEM_BYTES = FWD_SMEM_BYTES;
 
 // standard 8th-order central second-derivative weights (unscaled; h^-2 is folded into the coefficients)
 #define HV_A0 (-205.0f / 72.0f)

@@ -116,16 +116,15 @@ __device__ __forceinline__ bool tile_is_interior(const Geo& g, int x0, int z0) {
 
 struct FwdParams {
   Geo g;
-  float* pool;            // field planes; plane index = ((s_local * nslot) + slot) * 2 + parity
-  int nslot;
+  int nslot;              // pool plane index = ((s_local * nslot) + slot) * 2 + parity
+  float* pool;
   int n;                  // this launch computes level n+1 from levels n, n-1
   int bg_slot;            // slot of the background u
-  int bg_update;          // write u^{n+1}? (always 1 except sampling-only use)
+  int bg_update;          // write u^{n+1}? (1; 0 = sampling-only use)
   int born_slot0;         // Born field k lives in slot born_slot0 + k
   int K;                  // Born fields
   int FG, G;              // Born fields per CTA, CTAs (groups) per shot and tile
   const float* W2;        // [Nz][P]   dt^2 v^2 / h^2 (0 outside the padded grid)
-  const float* Q;         // [K][Nz][P] 2 dt^2 v dv_k / h^2 (0 in the sponge)
   const float* imgc;      // [nz][PI]  2 dt^2 / (v h^2); with s_out: store s^n = imgc * Lu^n
   float* s_out;           // level-n slot of the imaging-factor store for s_local = 0, or null
   long long s_shot_stride;
@@ -142,11 +141,42 @@ struct FwdParams {
   float* d_born;          // [S][K][nt][nrec] Born data (batch-local) or null
 };
 
-__global__ void __launch_bounds__(NTHREADS) fwd_step_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                            const FwdParams p) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* tiles = reinterpret_cast<float*>(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + NSTAGE * TILE_BYTES);
+// Per-point damping factors of this thread's points (SP: the tile touches the sponge).
+template <bool SP>
+struct Damp {
+  float cm[RZ][4], ci[RZ][4];
+  __device__ __forceinline__ void init(const Geo& g, int I0, int J0) {
+#pragma unroll
+    for (int r = 0; r < RZ; ++r)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float c = sponge_c(g, I0 + r, J0 + i);
+        cm[r][i] = 1.0f - c;
+        ci[r][i] = 1.0f / (1.0f + c);
+      }
+  }
+  // [2 C - (1 - c) prev + rhs] / (1 + c)
+  __device__ __forceinline__ float upd(int r, int i, float C, float prev, float rhs) const {
+    return (fmaf(2.0f, C, rhs) - cm[r][i] * prev) * ci[r][i];
+  }
+};
+template <>
+struct Damp<false> {
+  __device__ __forceinline__ void init(const Geo&, int, int) {}
+  __device__ __forceinline__ float upd(int, int, float C, float prev, float rhs) const {
+    return fmaf(2.0f, C, rhs) - prev;
+  }
+};
+
+template <bool SP>
+__device__ __forceinline__ float dmp_ci(const Damp<SP>& d, int r, int i) {
+  if constexpr (SP) return d.ci[r][i];
+  else return 1.0f;
+}
+
+template <bool SP>
+__device__ __forceinline__ void fwd_body(const CUtensorMap* mh, const CUtensorMap* mt, const CUtensorMap* mq,
+                                         const FwdParams& p, float* stages, uint64_t* bars) {
   const Geo& g = p.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
   const int x0 = blockIdx.x * TX, z0 = blockIdx.y * TZ;
@@ -157,96 +187,87 @@ __global__ void __launch_bounds__(NTHREADS) fwd_step_kernel(const __grid_constan
   const int par_n = p.n & 1, par_new = par_n ^ 1;
   const bool leader = (grp == 0) && p.bg_update;
   const long long shot_planes = static_cast<long long>(sl) * p.nslot;
-
-  if (tid == 0) {
-    tma_prefetch_desc(&tmap);
-    for (int i = 0; i < NSTAGE; ++i) mbar_init(&bars[i], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
   auto slot_of = [&](int item) { return item == 0 ? p.bg_slot : p.born_slot0 + fb + item - 1; };
+  // item inputs: halo of level n, tile of level n-1 (when updating), tile of q_k (Born items)
+  auto issue = [&](int item) {
+    const int stage = item % NSTAGE;
+    float* st = stages + stage * FWD_STAGE_FLOATS;
+    const bool upd = item > 0 || leader;
+    const uint32_t bytes = TILE_BYTES + (upd ? PT_BYTES : 0) + (item > 0 ? PT_BYTES : 0);
+    const int pl = static_cast<int>((shot_planes + slot_of(item)) * 2);
+    mbar_expect_tx(&bars[stage], bytes);
+    tma_load_3d(st, mh, &bars[stage], x0 - R, z0 - R, pl + par_n);
+    if (upd) tma_load_3d(st + TILE_FLOATS, mt, &bars[stage], x0, z0, pl + par_new);
+    if (item > 0) tma_load_3d(st + TILE_FLOATS + PT_FLOATS, mq, &bars[stage], x0, z0, fb + item - 1);
+  };
   if (tid == 0) {
-    for (int i = 0; i < min(NSTAGE, nitems); ++i) {
-      mbar_expect_tx(&bars[i], TILE_BYTES);
-      tma_load_3d(tiles + i * TILE_FLOATS, &tmap, &bars[i], x0 - R, z0 - R,
-                  static_cast<int>((shot_planes + slot_of(i)) * 2 + par_n));
-    }
+    for (int i = 0; i < min(NSTAGE, nitems); ++i) issue(i);
   }
 
-  const int lz0 = ty * RZ;
-  const int I0 = z0 + lz0;
+  const int I0 = z0 + ty * RZ;
   const int J0 = x0 + tx * 4;
-  const bool interior = tile_is_interior(g, x0, z0);
-  // per-point coefficients: w = dt^2 v^2 / h^2, (1 - c), 1 / (1 + c)
-  float w[RZ][4], cm[RZ][4], ci[RZ][4];
+  float w[RZ][4];
 #pragma unroll
   for (int r = 0; r < RZ; ++r) {
-    const int I = I0 + r;
-    float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (I < g.Nz) wv = ldg4(p.W2 + static_cast<long long>(I) * g.P + J0);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      w[r][i] = f4(wv, i);
-      const float c = interior ? 0.f : sponge_c(g, I, J0 + i);
-      cm[r][i] = 1.0f - c;
-      ci[r][i] = 1.0f / (1.0f + c);
-    }
+    const int I = min(I0 + r, g.Nz - 1);
+    const float4 wv = ldg4(p.W2 + static_cast<long long>(I) * g.P + J0);
+    w[r][0] = wv.x, w[r][1] = wv.y, w[r][2] = wv.z, w[r][3] = wv.w;
   }
+  Damp<SP> dmp;
+  dmp.init(g, I0, J0);
   const int tile_id = blockIdx.y * g.ntx + blockIdx.x;
   const int rb = p.trec_beg[tile_id], re = p.trec_beg[tile_id + 1];
   const int shot = p.shot0 + sl;
   const int sI = p.src_I[shot], sJ = p.src_J[shot];
   const float amp = p.src_amp[p.n];
+  const bool src_here = leader && sI >= I0 && sI < I0 + RZ && sJ >= J0 && sJ < J0 + 4;
 
   float Lb[RZ][4];
   for (int item = 0; item < nitems; ++item) {
     const int stage = item % NSTAGE;
+    const float* st = stages + stage * FWD_STAGE_FLOATS;
     const int slot = slot_of(item);
-    const long long new_plane = (shot_planes + slot) * 2 + par_new;
-    float* __restrict__ dst = p.pool + new_plane * g.plane;
-    // pointwise streams first (latency overlaps the TMA wait): u^{n-1} (same plane as u^{n+1}) and q_k
-    float4 prev[RZ], qv[RZ];
-    const bool do_update = (item > 0) || leader;
-    const float* qk = (item > 0) ? p.Q + static_cast<long long>(fb + item - 1) * g.plane : nullptr;
-#pragma unroll
-    for (int r = 0; r < RZ; ++r) {
-      const int I = I0 + r;
-      prev[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-      qv[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (do_update && I < g.Nz) {
-        prev[r] = ld4(dst + static_cast<long long>(I) * g.P + J0);
-        if (item > 0) qv[r] = ldg4(qk + static_cast<long long>(I) * g.P + J0);
-      }
-    }
+    const bool upd = item > 0 || leader;
     mbar_wait(&bars[stage], (item / NSTAGE) & 1);
-    const float* t = tiles + stage * TILE_FLOATS;
     float L[RZ][4], C[RZ][4];
-    lap_points(t, tx, ty, L, C);
+    lap_points(st, tx, ty, L, C);
     if (item == 0) {
 #pragma unroll
       for (int r = 0; r < RZ; ++r)
 #pragma unroll
         for (int i = 0; i < 4; ++i) Lb[r][i] = L[r][i];
     }
-    if (do_update) {
+    if (upd) {
+      float* __restrict__ dst = p.pool + ((shot_planes + slot) * 2 + par_new) * g.plane;
 #pragma unroll
       for (int r = 0; r < RZ; ++r) {
         const int I = I0 + r;
-        if (I >= g.Nz) continue;
-        float o[4];
+        const int o = (ty * RZ + r) * TX + tx * 4;
+        const float4 pv = ld4(st + TILE_FLOATS + o);
+        float4 qv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (item > 0) qv = ld4(st + TILE_FLOATS + PT_FLOATS + o);
+        float v[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int J = J0 + i;
           float rhs = w[r][i] * L[r][i];
-          if (item > 0) rhs = fmaf(f4(qv[r], i), Lb[r][i], rhs);
-          else if (I == sI && J == sJ) rhs += amp;
-          float v = (2.0f * C[r][i] - cm[r][i] * f4(prev[r], i) + rhs) * ci[r][i];
-          o[i] = (J < g.Nx) ? v : 0.0f;
+          if (item > 0) rhs = fmaf(f4(qv, i), Lb[r][i], rhs);
+          v[i] = dmp.upd(r, i, C[r][i], f4(pv, i), rhs);
         }
-        st4(dst + static_cast<long long>(I) * g.P + J0, make_float4(o[0], o[1], o[2], o[3]));
+        if (item == 0 && src_here && I == sI) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (J0 + i == sJ) v[i] += amp * (SP ? dmp_ci(dmp, r, i) : 1.0f);
+        }
+        if (SP) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (J0 + i >= g.Nx) v[i] = 0.0f;
+          if (I >= g.Nz) continue;
+        }
+        st4(dst + static_cast<long long>(I) * g.P + J0, make_float4(v[0], v[1], v[2], v[3]));
       }
     }
-    // imaging-factor store s^n = 2 dt^2 / (v h^2) * L~u^n on the interior (FULL / replay segments)
+    // imaging-factor store s^n = 2 dt^2 / (v h^2) * L~u^n on the interior (FULL store / replay segments)
     if (item == 0 && leader && p.s_out != nullptr) {
       const int jc = J0 - g.c0;
       if (jc >= 0 && jc < g.PI) {
@@ -259,7 +280,7 @@ __global__ void __launch_bounds__(NTHREADS) fwd_step_kernel(const __grid_constan
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int ix = J0 + i - g.W;
-            o[i] = (ix >= 0 && ix < g.nx) ? f4(ic, i) * Lb[r][i] : 0.0f;
+            o[i] = (!SP || (ix >= 0 && ix < g.nx)) ? f4(ic, i) * Lb[r][i] : 0.0f;
           }
           st4(p.s_out + sl * p.s_shot_stride + static_cast<long long>(iz) * g.PI + jc,
               make_float4(o[0], o[1], o[2], o[3]));
@@ -278,26 +299,44 @@ __global__ void __launch_bounds__(NTHREADS) fwd_step_kernel(const __grid_constan
         for (int q = rb + tid; q < re; q += NTHREADS) {
           const int rid = p.trec_id[q];
           const int lz = p.rec_I[rid] - z0 + R, lx = p.rec_J[rid] - x0 + R;
-          out[static_cast<long long>(p.n) * g.nrec + rid] = t[lz * HX + lx];
+          out[static_cast<long long>(p.n) * g.nrec + rid] = st[lz * HX + lx];
         }
       }
     }
     __syncthreads();  // every thread is done with this stage
     if (tid == 0 && item + NSTAGE < nitems) {
       fence_proxy_async();
-      mbar_expect_tx(&bars[stage], TILE_BYTES);
-      tma_load_3d(tiles + stage * TILE_FLOATS, &tmap, &bars[stage], x0 - R, z0 - R,
-                  static_cast<int>((shot_planes + slot_of(item + NSTAGE)) * 2 + par_n));
+      issue(item + NSTAGE);
     }
   }
+}
+
+__global__ void __launch_bounds__(NTHREADS, 2)
+    fwd_step_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
+                    const __grid_constant__ CUtensorMap mq, const FwdParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stages = reinterpret_cast<float*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + NSTAGE * FWD_STAGE_FLOATS * 4);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    tma_prefetch_desc(&mh);
+    tma_prefetch_desc(&mt);
+    tma_prefetch_desc(&mq);
+    for (int i = 0; i < NSTAGE; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tile_is_interior(p.g, blockIdx.x * TX, blockIdx.y * TZ))
+    fwd_body<false>(&mh, &mt, &mq, p, stages, bars);
+  else
+    fwd_body<true>(&mh, &mt, &mq, p, stages, bars);
 }
 
 // ------------------------------------------------------------------------------------------------ backward
 
 struct BwdParams {
   Geo g;
-  float* pool;
   int nslot;
+  float* pool;
   int j;                  // computes lambda^j from lambda^{j+1} (halo) and lambda^{j+2} (pointwise)
   int update;             // compute lambda^j (j >= 2; lambda^1 is never used)
   int imaging;            // accumulate s^j lambda^{j+1} (j <= nt-2)
@@ -318,11 +357,9 @@ struct BwdParams {
   const int* rec_J;
 };
 
-__global__ void __launch_bounds__(NTHREADS) bwd_step_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                            const BwdParams p) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* tiles = reinterpret_cast<float*>(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + NSTAGE * TILE_BYTES);
+template <bool SP>
+__device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMap* mt, const BwdParams& p,
+                                         float* stages, uint64_t* bars) {
   const Geo& g = p.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
   const int x0 = blockIdx.x * TX, z0 = blockIdx.y * TZ;
@@ -333,83 +370,68 @@ __global__ void __launch_bounds__(NTHREADS) bwd_step_kernel(const __grid_constan
   if (nitems <= 0) return;
   const int par_in = (p.j + 1) & 1, par_out = p.j & 1;
   const long long shot_planes = static_cast<long long>(sl) * p.nslot;
-
+  auto issue = [&](int item) {
+    const int stage = item % NSTAGE;
+    float* st = stages + stage * BWD_STAGE_FLOATS;
+    const int pl = static_cast<int>((shot_planes + p.slot0 + fb + item) * 2);
+    mbar_expect_tx(&bars[stage], TILE_BYTES + (p.update ? PT_BYTES : 0));
+    tma_load_3d(st, mh, &bars[stage], x0 - R, z0 - R, pl + par_in);
+    if (p.update) tma_load_3d(st + TILE_FLOATS, mt, &bars[stage], x0, z0, pl + par_out);
+  };
   if (tid == 0) {
-    tma_prefetch_desc(&tmap);
-    for (int i = 0; i < NSTAGE; ++i) mbar_init(&bars[i], 1);
-    fence_mbar_init();
+    for (int i = 0; i < min(NSTAGE, nitems); ++i) issue(i);
   }
-  __syncthreads();
-  if (tid == 0) {
-    for (int i = 0; i < min(NSTAGE, nitems); ++i) {
-      mbar_expect_tx(&bars[i], TILE_BYTES);
-      tma_load_3d(tiles + i * TILE_FLOATS, &tmap, &bars[i], x0 - R, z0 - R,
-                  static_cast<int>((shot_planes + p.slot0 + fb + i) * 2 + par_in));
-    }
-  }
-  const int lz0 = ty * RZ;
-  const int I0 = z0 + lz0;
+  const int I0 = z0 + ty * RZ;
   const int J0 = x0 + tx * 4;
-  const bool interior = tile_is_interior(g, x0, z0);
-  float w[RZ][4], cm[RZ][4], ci[RZ][4], sj[RZ][4];
+  float w[RZ][4], sj[RZ][4];
   const int jc = J0 - g.c0;
+  bool img_rows[RZ];
+  bool any_img = false;
 #pragma unroll
   for (int r = 0; r < RZ; ++r) {
     const int I = I0 + r;
-    float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (I < g.Nz) wv = ldg4(p.W2 + static_cast<long long>(I) * g.P + J0);
-    float4 sv = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 wv = ldg4(p.W2 + static_cast<long long>(min(I, g.Nz - 1)) * g.P + J0);
     const int iz = I - g.W;
-    if (p.imaging && iz >= 0 && iz < g.nz && jc >= 0 && jc < g.PI)
+    img_rows[r] = p.imaging && iz >= 0 && iz < g.nz && J0 + 3 >= g.W && J0 < g.W + g.nx;
+    any_img |= img_rows[r];
+    float4 sv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (img_rows[r] && jc >= 0 && jc < g.PI)
       sv = ldg4(p.s_lvl + sl * p.s_shot_stride + static_cast<long long>(iz) * g.PI + jc);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       w[r][i] = f4(wv, i);
       const int ix = J0 + i - g.W;
-      sj[r][i] = (ix >= 0 && ix < g.nx) ? f4(sv, i) : 0.0f;
-      const float c = interior ? 0.f : sponge_c(g, I, J0 + i);
-      cm[r][i] = 1.0f - c;
-      ci[r][i] = 1.0f / (1.0f + c);
+      sj[r][i] = (!SP || (ix >= 0 && ix < g.nx)) ? f4(sv, i) : 0.0f;
     }
   }
-  bool img_rows[RZ];
-  bool any_img = false;
-#pragma unroll
-  for (int r = 0; r < RZ; ++r) {
-    const int iz = I0 + r - g.W;
-    img_rows[r] = p.imaging && iz >= 0 && iz < g.nz && J0 + 3 >= g.W && J0 < g.W + g.nx;
-    any_img |= img_rows[r];
-  }
+  Damp<SP> dmp;
+  dmp.init(g, I0, J0);
   const int tile_id = blockIdx.y * g.ntx + blockIdx.x;
   const int rb = p.trec_beg[tile_id], re = p.trec_beg[tile_id + 1];
 
   for (int item = 0; item < nitems; ++item) {
     const int stage = item % NSTAGE;
+    const float* st = stages + stage * BWD_STAGE_FLOATS;
     const int slot = p.slot0 + fb + item;
     float* __restrict__ dst = p.pool + ((shot_planes + slot) * 2 + par_out) * g.plane;
-    float4 prev[RZ];
-#pragma unroll
-    for (int r = 0; r < RZ; ++r) {
-      const int I = I0 + r;
-      prev[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (p.update && I < g.Nz) prev[r] = ld4(dst + static_cast<long long>(I) * g.P + J0);
-    }
     mbar_wait(&bars[stage], (item / NSTAGE) & 1);
-    const float* t = tiles + stage * TILE_FLOATS;
     float L[RZ][4], C[RZ][4];
-    lap_points(t, tx, ty, L, C);
+    lap_points(st, tx, ty, L, C);
     if (p.update) {
 #pragma unroll
       for (int r = 0; r < RZ; ++r) {
         const int I = I0 + r;
-        if (I >= g.Nz) continue;
-        float o[4];
+        const float4 pv = ld4(st + TILE_FLOATS + (ty * RZ + r) * TX + tx * 4);
+        float v[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float v = (2.0f * C[r][i] - cm[r][i] * f4(prev[r], i) + w[r][i] * L[r][i]) * ci[r][i];
-          o[i] = (J0 + i < g.Nx) ? v : 0.0f;
+        for (int i = 0; i < 4; ++i) v[i] = dmp.upd(r, i, C[r][i], f4(pv, i), w[r][i] * L[r][i]);
+        if (SP) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (J0 + i >= g.Nx) v[i] = 0.0f;
+          if (I >= g.Nz) continue;
         }
-        st4(dst + static_cast<long long>(I) * g.P + J0, make_float4(o[0], o[1], o[2], o[3]));
+        st4(dst + static_cast<long long>(I) * g.P + J0, make_float4(v[0], v[1], v[2], v[3]));
       }
     }
     if (any_img) {  // zero-lag imaging: acc += s^j * lambda^{j+1} (RED.128: one writer per address per step)
@@ -425,9 +447,7 @@ __global__ void __launch_bounds__(NTHREADS) bwd_step_kernel(const __grid_constan
     __syncthreads();  // stage consumed and lambda^j of this tile stored
     if (tid == 0 && item + NSTAGE < nitems) {
       fence_proxy_async();
-      mbar_expect_tx(&bars[stage], TILE_BYTES);
-      tma_load_3d(tiles + stage * TILE_FLOATS, &tmap, &bars[stage], x0 - R, z0 - R,
-                  static_cast<int>((shot_planes + slot + NSTAGE) * 2 + par_in));
+      issue(item + NSTAGE);
     }
     // receiver injection into lambda^j: += v^2 / (1 + c) * rho[j][r]   (R^T scatter-add)
     if (p.update && re > rb) {
@@ -441,6 +461,25 @@ __global__ void __launch_bounds__(NTHREADS) bwd_step_kernel(const __grid_constan
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(NTHREADS, 2)
+    bwd_step_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
+                    const BwdParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stages = reinterpret_cast<float*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + NSTAGE * BWD_STAGE_FLOATS * 4);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    tma_prefetch_desc(&mh);
+    tma_prefetch_desc(&mt);
+    for (int i = 0; i < NSTAGE; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tile_is_interior(p.g, blockIdx.x * TX, blockIdx.y * TZ))
+    bwd_body<false>(&mh, &mt, p, stages, bars);
+  else
+    bwd_body<true>(&mh, &mt, p, stages, bars);
 }
 
 // ------------------------------------------------------------------------------------------------ helpers

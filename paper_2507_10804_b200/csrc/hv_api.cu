@@ -76,12 +76,11 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
   double budget = c->cfg.mem_budget ? static_cast<double>(c->cfg.mem_budget) : 0.9 * static_cast<double>(freeb);
   // shared (not per shot): Q, W2, imgc, rec coef, staging of V/HV/m
   const double shared = F4 * (static_cast<double>(K) * g.plane * 2 + g.plane + g.iplane + 4.0 * K * g.nz * g.nx +
-                              2.0 * g.nz * g.nx) + (1 << 20);
+                              2.0 * g.nz * g.nx + (double)pl->nacc * g.plane) + (1 << 20);
   auto per_shot = [&](int store, int k) {
     double b = F4 * 2.0 * pl->nslot * g.plane;                                  // field pool
     b += F4 * (double)K * g.nt * g.nrec;                                        // Born data
     if (grad) b += F4 * 2.0 * g.nt * g.nrec;                                    // data + residual
-    b += F4 * (double)pl->nacc * g.plane;                                       // accumulators
     if (adjoint) {
       if (store == HV_STORE_FULL) b += F4 * (double)g.nt * g.iplane;
       else b += F4 * (2.0 * ((g.nt - 1 + k - 1) / k) * g.plane + (double)k * g.iplane);
@@ -107,12 +106,9 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
                                   " GB per shot in flight; budget " + std::to_string(budget / 1e9) + " GB");
   int S = c->cfg.shot_batch > 0 ? c->cfg.shot_batch : 0;
   const int ntiles = g.ntx * g.ntz;
-  pl->FG = c->cfg.field_group > 0 ? c->cfg.field_group : 8;
-  if (S <= 0) {
-    const int G = std::max(1, (K + pl->FG - 1) / pl->FG);
-    const int ctas_per_shot = ntiles * G;
-    S = std::max(1, (148 * 4 + ctas_per_shot - 1) / ctas_per_shot);  // about 4 resident CTAs per SM
-  }
+  pl->FG = std::min(FWD_FG_MAX, c->cfg.field_group > 0 ? c->cfg.field_group : 6);
+  (void)ntiles;
+  if (S <= 0) S = 32;  // every CTA loops over the batch's shots: more shots amortise q_k loads and imaging writes
   S = std::min(S, fit);
   S = std::min(S, c->nloc);
   pl->S = std::max(1, S);
@@ -206,8 +202,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     if ((st = ws_get(c, "rres", sizeof(float) * (size_t)S * g.nt * g.nrec, (void**)&rres))) return st;
   }
   if (adjoint) {
-    if ((st = ws_get(c, "acc", sizeof(float) * g.plane * pl.nacc * S, (void**)&acc))) return st;
-    CU_TRY(cudaMemsetAsync(acc, 0, sizeof(float) * g.plane * pl.nacc * S, c->stream));
+    if ((st = ws_get(c, "acc", sizeof(float) * g.plane * pl.nacc, (void**)&acc))) return st;
+    CU_TRY(cudaMemsetAsync(acc, 0, sizeof(float) * g.plane * pl.nacc, c->stream));
     if (pl.store == HV_STORE_FULL) {
       if ((st = ws_get(c, "store", sizeof(float) * g.iplane * g.nt * S, (void**)&store))) return st;
     } else {
@@ -226,7 +222,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   const int Gf = K > 0 ? (K + FG - 1) / FG : 1;
   const int Fb = (grad ? 1 : 0) + K;  // adjoint fields
   const int slot0_b = grad ? 0 : 1;
-  const int Gb = std::max(1, (Fb + FG - 1) / FG);
+  const int Gb = std::max(1, (Fb + BWD_FG - 1) / BWD_FG);
+  const int fwd_smem = fwd_smem_bytes(K > 0 ? std::min(FG, K) : 0);
   const dim3 block(BX, BY);
   const dim3 tiles(g.ntx, g.ntz);
   double ms_f = 0, ms_b = 0;
@@ -254,7 +251,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     fp.born_slot0 = 1;
     fp.K = K;
     fp.FG = FG;
-    fp.G = Gf;
+    fp.S = Sb;
     fp.W2 = W2;
     fp.imgc = imgc;
     fp.shot0 = b0;
@@ -275,7 +272,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     }
     const bool full = adjoint && pl.store == HV_STORE_FULL;
     fp.s_shot_stride = full ? g.iplane * g.nt : 0;
-    const dim3 gridf(g.ntx, g.ntz, Sb * Gf);
+    const dim3 gridf(g.ntx, g.ntz, Gf);
     for (int n = 0; n <= g.nt - 2; ++n) {
       if (adjoint && pl.store == HV_STORE_CHECKPOINT && n % pl.k == 0) {
         // save (u^n, u^{n-1}): both parity planes of slot 0, per shot; layout ckpt[S][nck][2][plane]
@@ -286,7 +283,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
       }
       fp.n = n;
       fp.s_out = full ? store + (size_t)n * g.iplane : nullptr;
-      fwd_step_kernel<<<gridf, block, FWD_SMEM_BYTES, c->stream>>>(map_halo, map_tile, map_q, fp);
+      fwd_step_kernel<<<gridf, block, fwd_smem, c->stream>>>(map_halo, map_tile, map_q, fp);
       launches++;
     }
     CU_TRY(cudaEventRecord(e_f1, c->stream));
@@ -311,11 +308,9 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
       bp.nslot = nslot;
       bp.slot0 = slot0_b;
       bp.F = Fb;
-      bp.FG = FG;
-      bp.G = Gb;
+      bp.S = Sb;
       bp.W2 = W2;
       bp.acc = acc;
-      bp.nacc = pl.nacc;
       bp.rho_res = rres;
       bp.rho_born = dborn;
       bp.Kb = K;
@@ -324,7 +319,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
       bp.trec_id = c->d_trec_id;
       bp.rec_I = c->d_recI;
       bp.rec_J = c->d_recJ;
-      const dim3 gridb(g.ntx, g.ntz, Sb * Gb);
+      const dim3 gridb(g.ntx, g.ntz, Gb);
       CU_TRY(cudaEventRecord(e_b0, c->stream));
       int cur_b = -1;
       for (int j = g.nt - 1; j >= 1; --j) {
@@ -346,15 +341,14 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
               FwdParams rp = fp;
               rp.bg_slot = replay_slot;
               rp.K = 0;
-              rp.G = 1;
               rp.d_bg = nullptr;
               rp.d_born = nullptr;
               rp.s_shot_stride = g.iplane * pl.k;
-              const dim3 gridr(g.ntx, g.ntz, Sb);
+              const dim3 gridr(g.ntx, g.ntz, 1);
               for (int n = b; n < e; ++n) {
                 rp.n = n;
                 rp.s_out = seg + (size_t)(n - b) * g.iplane;
-                fwd_step_kernel<<<gridr, block, FWD_SMEM_BYTES, c->stream>>>(map_halo, map_tile, map_q, rp);
+                fwd_step_kernel<<<gridr, block, fwd_smem_bytes(0), c->stream>>>(map_halo, map_tile, map_q, rp);
                 launches++;
               }
               cur_b = b;
@@ -375,13 +369,13 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
 
   // --- a8 (within the GPU): fixed-order sum over the shots in flight, into the caller's layout
   if (grad) {
-    finalize_kernel<<<grid1d((long long)g.nz * g.nx), 256, 0, c->stream>>>(g, acc, S, pl.nacc, 0, 1,
+    finalize_kernel<<<grid1d((long long)g.nz * g.nx), 256, 0, c->stream>>>(g, acc, 1, pl.nacc, 0, 1,
                                                                              reinterpret_cast<float*>(o_g.dev));
     launches++;
   }
   if (K > 0) {
     finalize_kernel<<<grid1d((long long)K * g.nz * g.nx), 256, 0, c->stream>>>(
-        g, acc, S, pl.nacc, 1, K, reinterpret_cast<float*>(o_hv.dev));
+        g, acc, 1, pl.nacc, 1, K, reinterpret_cast<float*>(o_hv.dev));
     launches++;
   }
   CU_TRY(cudaGetLastError());
@@ -538,7 +532,8 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
     return HV_ECUDA;
   }
   c->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  if (cudaFuncSetAttribute(fwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FWD_SMEM_BYTES) !=
+  if (cudaFuncSetAttribute(fwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           fwd_smem_bytes(FWD_FG_MAX)) !=
           cudaSuccess ||
       cudaFuncSetAttribute(bwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_BYTES) !=
           cudaSuccess) {

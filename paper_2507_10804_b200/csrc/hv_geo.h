@@ -17,13 +17,16 @@ constexpr int TILE_BYTES = TILE_FLOATS * 4;
 constexpr int PT_FLOATS = TX * TZ;            // pointwise tile (no halo)
 constexpr int PT_BYTES = PT_FLOATS * 4;
 constexpr int NSTAGE = 3;                     // TMA pipeline depth (items in flight per CTA)
-// forward stage: halo u^n / du_k^n + tile u^{n-1} / du_k^{n-1} + tile q_k
-constexpr int FWD_STAGE_FLOATS = TILE_FLOATS + 2 * PT_FLOATS;
-constexpr int FWD_SMEM_BYTES = NSTAGE * FWD_STAGE_FLOATS * 4 + 64;
-// backward stage: halo lambda^{j+1} + tile lambda^{j+2}
-constexpr int BWD_STAGE_FLOATS = TILE_FLOATS + PT_FLOATS;
-constexpr int BWD_SMEM_BYTES = NSTAGE * BWD_STAGE_FLOATS * 4 + 64;
-constexpr int SMEM_BYTES = FWD_SMEM_BYTES;
+// one pipeline stage: halo of level n (stencil input) + pointwise tile of level n-1 (updated in place)
+constexpr int STAGE_FLOATS = TILE_FLOATS + PT_FLOATS;
+constexpr int STAGES_BYTES = NSTAGE * STAGE_FLOATS * 4;
+constexpr int BAR_BYTES = 128;              // keeps the q tiles behind the barriers 128-byte aligned (TMA)
+// forward CTA: stages + the q_k tiles of its field group (loaded once, reused by every shot of the batch)
+constexpr int FWD_FG_MAX = 16;
+constexpr int fwd_smem_bytes(int fg) { return STAGES_BYTES + BAR_BYTES + fg * PT_BYTES; }
+// backward CTA: stages; its BWD_FG adjoint fields keep their imaging sums over the batch's shots in registers
+constexpr int BWD_FG = 4;
+constexpr int BWD_SMEM_BYTES = STAGES_BYTES + BAR_BYTES;
 
 // standard 8th-order central second-derivative weights (unscaled; h^-2 is folded into the coefficients)
 #define HV_A0 (-205.0f / 72.0f)

@@ -123,7 +123,8 @@ struct FwdParams {
   int bg_update;          // write u^{n+1}? (1; 0 = sampling-only use)
   int born_slot0;         // Born field k lives in slot born_slot0 + k
   int K;                  // Born fields
-  int FG, G;              // Born fields per CTA, CTAs (groups) per shot and tile
+  int FG;                 // Born fields per CTA (grid.z = field groups; every CTA loops over the S shots)
+  int S;                  // shots of the batch
   const float* W2;        // [Nz][P]   dt^2 v^2 / h^2 (0 outside the padded grid)
   const float* imgc;      // [nz][PI]  2 dt^2 / (v h^2); with s_out: store s^n = imgc * Lu^n
   float* s_out;           // level-n slot of the imaging-factor store for s_local = 0, or null
@@ -176,31 +177,35 @@ __device__ __forceinline__ float dmp_ci(const Damp<SP>& d, int r, int i) {
 
 template <bool SP>
 __device__ __forceinline__ void fwd_body(const CUtensorMap* mh, const CUtensorMap* mt, const CUtensorMap* mq,
-                                         const FwdParams& p, float* stages, uint64_t* bars) {
+                                         const FwdParams& p, float* stages, float* qs, uint64_t* bars) {
   const Geo& g = p.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
   const int x0 = blockIdx.x * TX, z0 = blockIdx.y * TZ;
-  const int sl = blockIdx.z / p.G, grp = blockIdx.z % p.G;
+  const int grp = blockIdx.z;
   const int fb = grp * p.FG;
-  const int fe = min(p.K, fb + p.FG);
-  const int nitems = 1 + max(0, fe - fb);
+  const int nf = max(0, min(p.K, fb + p.FG) - fb);   // Born fields of this CTA
+  const int ips = 1 + nf;                             // items per shot: background, then its Born fields
+  const int nitems = p.S * ips;
   const int par_n = p.n & 1, par_new = par_n ^ 1;
   const bool leader = (grp == 0) && p.bg_update;
-  const long long shot_planes = static_cast<long long>(sl) * p.nslot;
-  auto slot_of = [&](int item) { return item == 0 ? p.bg_slot : p.born_slot0 + fb + item - 1; };
-  // item inputs: halo of level n, tile of level n-1 (when updating), tile of q_k (Born items)
+  uint64_t* qbar = bars + NSTAGE;
+  // item inputs: halo of level n, tile of level n-1 (when this CTA updates the field)
   auto issue = [&](int item) {
     const int stage = item % NSTAGE;
-    float* st = stages + stage * FWD_STAGE_FLOATS;
-    const bool upd = item > 0 || leader;
-    const uint32_t bytes = TILE_BYTES + (upd ? PT_BYTES : 0) + (item > 0 ? PT_BYTES : 0);
-    const int pl = static_cast<int>((shot_planes + slot_of(item)) * 2);
-    mbar_expect_tx(&bars[stage], bytes);
+    const int s = item / ips, t = item % ips;
+    float* st = stages + stage * STAGE_FLOATS;
+    const bool upd = t > 0 || leader;
+    const int slot = t == 0 ? p.bg_slot : p.born_slot0 + fb + t - 1;
+    const int pl = (s * p.nslot + slot) * 2;
+    mbar_expect_tx(&bars[stage], TILE_BYTES + (upd ? PT_BYTES : 0));
     tma_load_3d(st, mh, &bars[stage], x0 - R, z0 - R, pl + par_n);
     if (upd) tma_load_3d(st + TILE_FLOATS, mt, &bars[stage], x0, z0, pl + par_new);
-    if (item > 0) tma_load_3d(st + TILE_FLOATS + PT_FLOATS, mq, &bars[stage], x0, z0, fb + item - 1);
   };
   if (tid == 0) {
+    if (nf > 0) {  // q_k tiles of the group, once for all shots
+      mbar_expect_tx(qbar, nf * PT_BYTES);
+      for (int t = 0; t < nf; ++t) tma_load_3d(qs + t * PT_FLOATS, mq, qbar, x0, z0, fb + t);
+    }
     for (int i = 0; i < min(NSTAGE, nitems); ++i) issue(i);
   }
 
@@ -217,46 +222,51 @@ __device__ __forceinline__ void fwd_body(const CUtensorMap* mh, const CUtensorMa
   dmp.init(g, I0, J0);
   const int tile_id = blockIdx.y * g.ntx + blockIdx.x;
   const int rb = p.trec_beg[tile_id], re = p.trec_beg[tile_id + 1];
-  const int shot = p.shot0 + sl;
-  const int sI = p.src_I[shot], sJ = p.src_J[shot];
   const float amp = p.src_amp[p.n];
-  const bool src_here = leader && sI >= I0 && sI < I0 + RZ && sJ >= J0 && sJ < J0 + 4;
+  if (nf > 0) mbar_wait(qbar, 0);
 
   float Lb[RZ][4];
+  int sI = -1, sJ = -1;
   for (int item = 0; item < nitems; ++item) {
     const int stage = item % NSTAGE;
-    const float* st = stages + stage * FWD_STAGE_FLOATS;
-    const int slot = slot_of(item);
-    const bool upd = item > 0 || leader;
+    const int s = item / ips, t = item % ips;
+    const float* st = stages + stage * STAGE_FLOATS;
+    const int slot = t == 0 ? p.bg_slot : p.born_slot0 + fb + t - 1;
+    const bool upd = t > 0 || leader;
+    if (t == 0) {
+      sI = p.src_I[p.shot0 + s];
+      sJ = p.src_J[p.shot0 + s];
+    }
     mbar_wait(&bars[stage], (item / NSTAGE) & 1);
     float L[RZ][4], C[RZ][4];
     lap_points(st, tx, ty, L, C);
-    if (item == 0) {
+    if (t == 0) {
 #pragma unroll
       for (int r = 0; r < RZ; ++r)
 #pragma unroll
         for (int i = 0; i < 4; ++i) Lb[r][i] = L[r][i];
     }
     if (upd) {
-      float* __restrict__ dst = p.pool + ((shot_planes + slot) * 2 + par_new) * g.plane;
+      float* __restrict__ dst = p.pool + (static_cast<long long>(s * p.nslot + slot) * 2 + par_new) * g.plane;
+      const float* qk = qs + (t > 0 ? t - 1 : 0) * PT_FLOATS;
 #pragma unroll
       for (int r = 0; r < RZ; ++r) {
         const int I = I0 + r;
         const int o = (ty * RZ + r) * TX + tx * 4;
         const float4 pv = ld4(st + TILE_FLOATS + o);
         float4 qv = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (item > 0) qv = ld4(st + TILE_FLOATS + PT_FLOATS + o);
+        if (t > 0) qv = ld4(qk + o);
         float v[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           float rhs = w[r][i] * L[r][i];
-          if (item > 0) rhs = fmaf(f4(qv, i), Lb[r][i], rhs);
+          if (t > 0) rhs = fmaf(f4(qv, i), Lb[r][i], rhs);
           v[i] = dmp.upd(r, i, C[r][i], f4(pv, i), rhs);
         }
-        if (item == 0 && src_here && I == sI) {
+        if (t == 0 && I == sI && sJ >= J0 && sJ < J0 + 4) {
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            if (J0 + i == sJ) v[i] += amp * (SP ? dmp_ci(dmp, r, i) : 1.0f);
+            if (J0 + i == sJ) v[i] += amp * dmp_ci(dmp, r, i);
         }
         if (SP) {
 #pragma unroll
@@ -268,7 +278,7 @@ __device__ __forceinline__ void fwd_body(const CUtensorMap* mh, const CUtensorMa
       }
     }
     // imaging-factor store s^n = 2 dt^2 / (v h^2) * L~u^n on the interior (FULL store / replay segments)
-    if (item == 0 && leader && p.s_out != nullptr) {
+    if (t == 0 && leader && p.s_out != nullptr) {
       const int jc = J0 - g.c0;
       if (jc >= 0 && jc < g.PI) {
 #pragma unroll
@@ -282,7 +292,7 @@ __device__ __forceinline__ void fwd_body(const CUtensorMap* mh, const CUtensorMa
             const int ix = J0 + i - g.W;
             o[i] = (!SP || (ix >= 0 && ix < g.nx)) ? f4(ic, i) * Lb[r][i] : 0.0f;
           }
-          st4(p.s_out + sl * p.s_shot_stride + static_cast<long long>(iz) * g.PI + jc,
+          st4(p.s_out + s * p.s_shot_stride + static_cast<long long>(iz) * g.PI + jc,
               make_float4(o[0], o[1], o[2], o[3]));
         }
       }
@@ -290,10 +300,10 @@ __device__ __forceinline__ void fwd_body(const CUtensorMap* mh, const CUtensorMa
     // receiver sampling of level n from the staged tile (d[n] = u^n[rec]; level nt-1 by gather_last_kernel)
     if (re > rb) {
       float* out = nullptr;
-      if (item == 0) {
-        if (leader && p.d_bg) out = p.d_bg + static_cast<long long>(p.dbg_shot0 + sl) * g.nt * g.nrec;
+      if (t == 0) {
+        if (leader && p.d_bg) out = p.d_bg + static_cast<long long>(p.dbg_shot0 + s) * g.nt * g.nrec;
       } else if (p.d_born) {
-        out = p.d_born + (static_cast<long long>(sl) * p.K + (fb + item - 1)) * g.nt * g.nrec;
+        out = p.d_born + (static_cast<long long>(s) * p.K + (fb + t - 1)) * g.nt * g.nrec;
       }
       if (out) {
         for (int q = rb + tid; q < re; q += NTHREADS) {
@@ -316,19 +326,20 @@ __global__ void __launch_bounds__(NTHREADS, 2)
                     const __grid_constant__ CUtensorMap mq, const FwdParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stages = reinterpret_cast<float*>(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + NSTAGE * FWD_STAGE_FLOATS * 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES_BYTES);
+  float* qs = reinterpret_cast<float*>(smem_raw + STAGES_BYTES + BAR_BYTES);
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     tma_prefetch_desc(&mh);
     tma_prefetch_desc(&mt);
     tma_prefetch_desc(&mq);
-    for (int i = 0; i < NSTAGE; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < NSTAGE + 1; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (tile_is_interior(p.g, blockIdx.x * TX, blockIdx.y * TZ))
-    fwd_body<false>(&mh, &mt, &mq, p, stages, bars);
+    fwd_body<false>(&mh, &mt, &mq, p, stages, qs, bars);
   else
-    fwd_body<true>(&mh, &mt, &mq, p, stages, bars);
+    fwd_body<true>(&mh, &mt, &mq, p, stages, qs, bars);
 }
 
 // ------------------------------------------------------------------------------------------------ backward
@@ -340,13 +351,12 @@ struct BwdParams {
   int j;                  // computes lambda^j from lambda^{j+1} (halo) and lambda^{j+2} (pointwise)
   int update;             // compute lambda^j (j >= 2; lambda^1 is never used)
   int imaging;            // accumulate s^j lambda^{j+1} (j <= nt-2)
-  int slot0, F;           // adjoint fields in slots slot0 .. slot0 + F - 1
-  int FG, G;
+  int slot0, F;           // adjoint fields in slots slot0 .. slot0 + F - 1; BWD_FG per CTA (grid.z)
+  int S;                  // shots of the batch (every CTA loops over them)
   const float* W2;
-  const float* s_lvl;     // s^j for s_local = 0
+  const float* s_lvl;     // s^j for batch shot 0
   long long s_shot_stride;
-  float* acc;             // [S][nacc][Nz][P], index by slot
-  int nacc;
+  float* acc;             // [nacc][Nz][P], index by slot (summed over shots and batches)
   const float* rho_res;   // slot 0 injection data [S][nt][nrec] (gradient), or null
   const float* rho_born;  // slot k >= 1 injection data [S][K][nt][nrec]
   int Kb;                 // K of rho_born
@@ -363,17 +373,16 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   const Geo& g = p.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
   const int x0 = blockIdx.x * TX, z0 = blockIdx.y * TZ;
-  const int sl = blockIdx.z / p.G, grp = blockIdx.z % p.G;
-  const int fb = grp * p.FG;
-  const int fe = min(p.F, fb + p.FG);
-  const int nitems = fe - fb;
-  if (nitems <= 0) return;
+  const int fb = blockIdx.z * BWD_FG;
+  const int nf = min(p.F, fb + BWD_FG) - fb;
+  if (nf <= 0) return;
+  const int nitems = p.S * nf;
   const int par_in = (p.j + 1) & 1, par_out = p.j & 1;
-  const long long shot_planes = static_cast<long long>(sl) * p.nslot;
   auto issue = [&](int item) {
     const int stage = item % NSTAGE;
-    float* st = stages + stage * BWD_STAGE_FLOATS;
-    const int pl = static_cast<int>((shot_planes + p.slot0 + fb + item) * 2);
+    const int s = item / nf, t = item % nf;
+    float* st = stages + stage * STAGE_FLOATS;
+    const int pl = (s * p.nslot + p.slot0 + fb + t) * 2;
     mbar_expect_tx(&bars[stage], TILE_BYTES + (p.update ? PT_BYTES : 0));
     tma_load_3d(st, mh, &bars[stage], x0 - R, z0 - R, pl + par_in);
     if (p.update) tma_load_3d(st + TILE_FLOATS, mt, &bars[stage], x0, z0, pl + par_out);
@@ -383,81 +392,115 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   }
   const int I0 = z0 + ty * RZ;
   const int J0 = x0 + tx * 4;
-  float w[RZ][4], sj[RZ][4];
   const int jc = J0 - g.c0;
+  float w[RZ][4];
   bool img_rows[RZ];
   bool any_img = false;
 #pragma unroll
   for (int r = 0; r < RZ; ++r) {
     const int I = I0 + r;
     const float4 wv = ldg4(p.W2 + static_cast<long long>(min(I, g.Nz - 1)) * g.P + J0);
+    w[r][0] = wv.x, w[r][1] = wv.y, w[r][2] = wv.z, w[r][3] = wv.w;
     const int iz = I - g.W;
-    img_rows[r] = p.imaging && iz >= 0 && iz < g.nz && J0 + 3 >= g.W && J0 < g.W + g.nx;
+    img_rows[r] = p.imaging && iz >= 0 && iz < g.nz && J0 + 3 >= g.W && J0 < g.W + g.nx && jc >= 0 &&
+                  jc < g.PI;
     any_img |= img_rows[r];
-    float4 sv = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (img_rows[r] && jc >= 0 && jc < g.PI)
-      sv = ldg4(p.s_lvl + sl * p.s_shot_stride + static_cast<long long>(iz) * g.PI + jc);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      w[r][i] = f4(wv, i);
-      const int ix = J0 + i - g.W;
-      sj[r][i] = (!SP || (ix >= 0 && ix < g.nx)) ? f4(sv, i) : 0.0f;
-    }
   }
+  // imaging factor s^j of shot s for this thread's points (prefetched one shot ahead)
+  auto load_sj = [&](int s, float4 (&dst)[RZ]) {
+#pragma unroll
+    for (int r = 0; r < RZ; ++r) {
+      dst[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (img_rows[r])
+        dst[r] = ldg4(p.s_lvl + s * p.s_shot_stride + static_cast<long long>(I0 + r - g.W) * g.PI + jc);
+    }
+  };
+  float4 snext[RZ];
+  load_sj(0, snext);
   Damp<SP> dmp;
   dmp.init(g, I0, J0);
   const int tile_id = blockIdx.y * g.ntx + blockIdx.x;
   const int rb = p.trec_beg[tile_id], re = p.trec_beg[tile_id + 1];
+  float acc[BWD_FG][RZ][4];
+#pragma unroll
+  for (int t = 0; t < BWD_FG; ++t)
+#pragma unroll
+    for (int r = 0; r < RZ; ++r)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[t][r][i] = 0.0f;
 
-  for (int item = 0; item < nitems; ++item) {
-    const int stage = item % NSTAGE;
-    const float* st = stages + stage * BWD_STAGE_FLOATS;
-    const int slot = p.slot0 + fb + item;
-    float* __restrict__ dst = p.pool + ((shot_planes + slot) * 2 + par_out) * g.plane;
-    mbar_wait(&bars[stage], (item / NSTAGE) & 1);
-    float L[RZ][4], C[RZ][4];
-    lap_points(st, tx, ty, L, C);
-    if (p.update) {
+  for (int s = 0; s < p.S; ++s) {
+    float sj[RZ][4];
 #pragma unroll
-      for (int r = 0; r < RZ; ++r) {
-        const int I = I0 + r;
-        const float4 pv = ld4(st + TILE_FLOATS + (ty * RZ + r) * TX + tx * 4);
-        float v[4];
+    for (int r = 0; r < RZ; ++r) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = dmp.upd(r, i, C[r][i], f4(pv, i), w[r][i] * L[r][i]);
-        if (SP) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (J0 + i >= g.Nx) v[i] = 0.0f;
-          if (I >= g.Nz) continue;
-        }
-        st4(dst + static_cast<long long>(I) * g.P + J0, make_float4(v[0], v[1], v[2], v[3]));
+      for (int i = 0; i < 4; ++i) {
+        const int ix = J0 + i - g.W;
+        sj[r][i] = (!SP || (ix >= 0 && ix < g.nx)) ? f4(snext[r], i) : 0.0f;
       }
     }
-    if (any_img) {  // zero-lag imaging: acc += s^j * lambda^{j+1} (RED.128: one writer per address per step)
-      float* a = p.acc + (static_cast<long long>(sl) * p.nacc + slot) * g.plane;
+    if (any_img && s + 1 < p.S) load_sj(s + 1, snext);
+#pragma unroll
+    for (int t = 0; t < BWD_FG; ++t) {
+      if (t >= nf) break;
+      const int item = s * nf + t;
+      const int stage = item % NSTAGE;
+      const float* st = stages + stage * STAGE_FLOATS;
+      const int slot = p.slot0 + fb + t;
+      float* __restrict__ dst = p.pool + (static_cast<long long>(s * p.nslot + slot) * 2 + par_out) * g.plane;
+      mbar_wait(&bars[stage], (item / NSTAGE) & 1);
+      float L[RZ][4], C[RZ][4];
+      lap_points(st, tx, ty, L, C);
+      if (p.update) {
+#pragma unroll
+        for (int r = 0; r < RZ; ++r) {
+          const int I = I0 + r;
+          const float4 pv = ld4(st + TILE_FLOATS + (ty * RZ + r) * TX + tx * 4);
+          float v[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[i] = dmp.upd(r, i, C[r][i], f4(pv, i), w[r][i] * L[r][i]);
+          if (SP) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (J0 + i >= g.Nx) v[i] = 0.0f;
+            if (I >= g.Nz) continue;
+          }
+          st4(dst + static_cast<long long>(I) * g.P + J0, make_float4(v[0], v[1], v[2], v[3]));
+        }
+      }
+      // zero-lag imaging, summed over the batch's shots in registers: acc += s^j * lambda^{j+1}
+#pragma unroll
+      for (int r = 0; r < RZ; ++r)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[t][r][i] = fmaf(sj[r][i], C[r][i], acc[t][r][i]);
+      __syncthreads();  // stage consumed and lambda^j of this tile stored
+      if (tid == 0 && item + NSTAGE < nitems) {
+        fence_proxy_async();
+        issue(item + NSTAGE);
+      }
+      // receiver injection into lambda^j: += v^2 / (1 + c) * rho[j][r]   (R^T scatter-add)
+      if (p.update && re > rb) {
+        const float* rho = (slot == 0)
+                               ? p.rho_res + static_cast<long long>(s) * g.nt * g.nrec
+                               : p.rho_born + (static_cast<long long>(s) * p.Kb + (slot - 1)) * g.nt * g.nrec;
+        for (int q = rb + tid; q < re; q += NTHREADS) {
+          const int rid = p.trec_id[q];
+          const float val = p.rec_coef[rid] * rho[static_cast<long long>(p.j) * g.nrec + rid];
+          atomicAdd(dst + static_cast<long long>(p.rec_I[rid]) * g.P + p.rec_J[rid], val);
+        }
+      }
+    }
+  }
+  if (any_img) {  // one writer per (field, point) per step: RED.128, deterministic order over steps
+#pragma unroll
+    for (int t = 0; t < BWD_FG; ++t) {
+      if (t >= nf) break;
+      float* a = p.acc + static_cast<long long>(p.slot0 + fb + t) * g.plane;
 #pragma unroll
       for (int r = 0; r < RZ; ++r) {
         if (!img_rows[r]) continue;
-        const float4 add = make_float4(sj[r][0] * C[r][0], sj[r][1] * C[r][1], sj[r][2] * C[r][2],
-                                       sj[r][3] * C[r][3]);
-        atomicAdd(reinterpret_cast<float4*>(a + static_cast<long long>(I0 + r) * g.P + J0), add);
-      }
-    }
-    __syncthreads();  // stage consumed and lambda^j of this tile stored
-    if (tid == 0 && item + NSTAGE < nitems) {
-      fence_proxy_async();
-      issue(item + NSTAGE);
-    }
-    // receiver injection into lambda^j: += v^2 / (1 + c) * rho[j][r]   (R^T scatter-add)
-    if (p.update && re > rb) {
-      const float* rho = (slot == 0)
-                             ? p.rho_res + static_cast<long long>(sl) * g.nt * g.nrec
-                             : p.rho_born + (static_cast<long long>(sl) * p.Kb + (slot - 1)) * g.nt * g.nrec;
-      for (int q = rb + tid; q < re; q += NTHREADS) {
-        const int rid = p.trec_id[q];
-        const float val = p.rec_coef[rid] * rho[static_cast<long long>(p.j) * g.nrec + rid];
-        atomicAdd(dst + static_cast<long long>(p.rec_I[rid]) * g.P + p.rec_J[rid], val);
+        atomicAdd(reinterpret_cast<float4*>(a + static_cast<long long>(I0 + r) * g.P + J0),
+                  make_float4(acc[t][r][0], acc[t][r][1], acc[t][r][2], acc[t][r][3]));
       }
     }
   }
@@ -468,7 +511,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
                     const BwdParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stages = reinterpret_cast<float*>(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + NSTAGE * BWD_STAGE_FLOATS * 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES_BYTES);
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     tma_prefetch_desc(&mh);
     tma_prefetch_desc(&mt);

@@ -54,13 +54,14 @@ def workload_counts(wl, K):
 
 
 def alg_bytes(wl, K, shots):
-    """Algorithmic fp32 HBM bytes per launch (FULL store): forward step reads u^n, u^{n-1}, w and
-    writes u^{n+1} (16 B / padded point), 16 B per Born field, writes the imaging factor (4 B / interior point);
-    backward step moves 20 B per adjoint field (lambda^{j+1}, lambda^{j+2}, HV read + lambda^j, HV write) plus w
-    (4 B / padded point) and the imaging factor (4 B / interior point)."""
+    """Algorithmic fp32 HBM bytes per launch = SURVEY.md §8(d) per-unit figures x units per launch:
+    forward step: a1 16 B + a2 16 B per Born field, per padded point, + FULL store write 4 B per interior point;
+    backward step: a5 + a7 20 B per adjoint field per padded point + FULL store read 4 B per interior point.
+    These are the bytes of a per-shot single-step scheme; the kernels share q_k and the imaging sums across the
+    shots of a launch, so they move fewer (the measured DRAM bytes are reported as `traffic`)."""
     Np, N, _ = workload_counts(wl, K)
     fwd = shots * (16.0 * Np * (1 + K) + 4.0 * N)
-    bwd = shots * (20.0 * Np * K + 4.0 * Np + 4.0 * N)
+    bwd = shots * (20.0 * Np * K + 4.0 * N)
     return fwd, bwd
 
 
@@ -203,13 +204,12 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
+    from paper_2507_10804_b200.dist import shard_range
+
     wl = W.config(args.config)
     K = wl.n_probes
     ns = wl.ns
-    per = ns // ws
-    extra = ns % ws
-    b = rank * per + min(rank, extra)
-    e = b + per + (1 if rank < extra else 0)
+    b, e = shard_range(ns, ws, rank)
     solver = hv.Solver.from_workload(wl, src_begin=b, src_end=e, device=local, store=args.store,
                                      shot_batch=args.shot_batch, field_group=args.field_group)
     V_h = wl.probes()
@@ -300,11 +300,15 @@ def main():
         kern = {"fwd_step_kernel": (fb, f_launch_ms), "bwd_step_kernel": (bb, b_launch_ms)}
         dom = max(kern, key=lambda k: kern[k][1])
         achieved = kern[dom][0] / (kern[dom][1] / 1000.0) / 1e9
-        traffic = None
+        traffic, traffic_src = None, None
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tpath):
             try:
-                traffic = json.load(open(tpath)).get(dom)
+                tj = json.load(open(tpath))
+                rec = tj.get(dom, {})
+                if rec.get("config") == {"workload": f"cfg{args.config}", "shot_batch": shots_per_batch,
+                                         "field_group": solver.stats()["field_group"]}:
+                    traffic, traffic_src = rec.get("dram_bytes_per_launch"), tj.get("source")
             except Exception:
                 traffic = None
         cpu = None
@@ -325,7 +329,9 @@ def main():
                        "shot_batch": shots_per_batch, "field_group": solver.stats()["field_group"]},
             "gpts_per_s": U / (ms_step / 1000.0) / 1e9,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "dram_frac": (traffic / (kern[dom][1] / 1000.0) / 1e9 / peak) if traffic else None,
+                         "peak_source": peak_src,
                          "alg_bytes_per_launch": kern[dom][0], "avg_launch_ms": kern[dom][1],
                          "kernels": {k: {"alg_bytes_per_launch": v[0], "avg_launch_ms": v[1],
                                          "achieved_gbs": v[0] / (v[1] / 1000.0) / 1e9}

@@ -21,7 +21,7 @@ import numpy as np
 __all__ = ["Solver", "HVError", "lib", "STORE", "psido_apply"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhv.so")
+LIB_PATH = os.environ.get("HV_LIB") or os.path.join(_HERE, "libhv.so")  # HV_LIB: tuning variants only
 
 HV_OK, HV_EINVAL, HV_EGRID, HV_ECFL, HV_ENOMEM, HV_ECUDA, HV_ESTATE = range(7)
 STATUS = {0: "HV_OK", 1: "HV_EINVAL", 2: "HV_EGRID", 3: "HV_ECFL", 4: "HV_ENOMEM", 5: "HV_ECUDA", 6: "HV_ESTATE"}

@@ -35,12 +35,14 @@ def _stale() -> bool:
     return False
 
 
-def build(force: bool = False, ptxas_verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, ptxas_verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Compile libhv.so (or a tuning variant `out` with -D`defines`)."""
+    if out == LIB and not force and not _stale():
         return LIB
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-fvisibility=hidden",
-           "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES],
+           *[f"-D{d}" for d in defines],
+           "-o", out + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES],
            "-lcufft", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     if ptxas_verbose:
         cmd.insert(1, "-Xptxas=-v")
@@ -49,8 +51,8 @@ def build(force: bool = False, ptxas_verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
     if ptxas_verbose:
         sys.stderr.write(r.stdout + r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -16,7 +16,13 @@ constexpr int TILE_FLOATS = HX * HZ;          // halo tile (stencil input)
 constexpr int TILE_BYTES = TILE_FLOATS * 4;
 constexpr int PT_FLOATS = TX * TZ;            // pointwise tile (no halo)
 constexpr int PT_BYTES = PT_FLOATS * 4;
-constexpr int NSTAGE = 3;                     // TMA pipeline depth (items in flight per CTA)
+#ifndef HV_NSTAGE
+#define HV_NSTAGE 3
+#endif
+#ifndef HV_BWD_FG
+#define HV_BWD_FG 2
+#endif
+constexpr int NSTAGE = HV_NSTAGE;             // TMA pipeline depth (items in flight per CTA)
 // one pipeline stage: halo of level n (stencil input) + pointwise tile of level n-1 (updated in place)
 constexpr int STAGE_FLOATS = TILE_FLOATS + PT_FLOATS;
 constexpr int STAGES_BYTES = NSTAGE * STAGE_FLOATS * 4;
@@ -25,7 +31,7 @@ constexpr int BAR_BYTES = 128;              // keeps the q tiles behind the barr
 constexpr int FWD_FG_MAX = 16;
 constexpr int fwd_smem_bytes(int fg) { return STAGES_BYTES + BAR_BYTES + fg * PT_BYTES; }
 // backward CTA: stages; its BWD_FG adjoint fields keep their imaging sums over the batch's shots in registers
-constexpr int BWD_FG = 4;
+constexpr int BWD_FG = HV_BWD_FG;
 constexpr int BWD_SMEM_BYTES = STAGES_BYTES + BAR_BYTES;
 
 // standard 8th-order central second-derivative weights (unscaled; h^-2 is folded into the coefficients)

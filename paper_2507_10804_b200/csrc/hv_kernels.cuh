@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "hv_geo.h"
 
 namespace hvk {
@@ -142,10 +144,10 @@ struct FwdParams {
   float* d_born;          // [S][K][nt][nrec] Born data (batch-local) or null
 };
 
-// Per-point damping factors of this thread's points (SP: the tile touches the sponge).
+// Per-point damping of this thread's points (SP: the tile touches the sponge): (1 - c) and 1 / (1 + c).
 template <bool SP>
 struct Damp {
-  float cm[RZ][4], ci[RZ][4];
+  float cm[RZ][4], ci_[RZ][4];
   __device__ __forceinline__ void init(const Geo& g, int I0, int J0) {
 #pragma unroll
     for (int r = 0; r < RZ; ++r)
@@ -153,14 +155,42 @@ struct Damp {
       for (int i = 0; i < 4; ++i) {
         const float c = sponge_c(g, I0 + r, J0 + i);
         cm[r][i] = 1.0f - c;
-        ci[r][i] = 1.0f / (1.0f + c);
+        ci_[r][i] = 1.0f / (1.0f + c);
       }
   }
+  __device__ __forceinline__ float ci(int r, int i) const { return ci_[r][i]; }
   // [2 C - (1 - c) prev + rhs] / (1 + c)
   __device__ __forceinline__ float upd(int r, int i, float C, float prev, float rhs) const {
-    return (fmaf(2.0f, C, rhs) - cm[r][i] * prev) * ci[r][i];
+    return (fmaf(2.0f, C, rhs) - cm[r][i] * prev) * ci_[r][i];
   }
 };
+// Register-lean variant (backward kernel, which also holds BWD_FG imaging sums): keeps c only and recomputes
+// 1 / (1 + c) correctly rounded (__frcp_rn == 1.0f / (1.0f + c), so both variants give identical bits).
+template <bool SP>
+struct DampLite {
+  float c[RZ][4];
+  __device__ __forceinline__ void init(const Geo& g, int I0, int J0) {
+#pragma unroll
+    for (int r = 0; r < RZ; ++r)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c[r][i] = sponge_c(g, I0 + r, J0 + i);
+  }
+  __device__ __forceinline__ float upd(int r, int i, float C, float prev, float rhs) const {
+    return (fmaf(2.0f, C, rhs) - (1.0f - c[r][i]) * prev) * __frcp_rn(1.0f + c[r][i]);
+  }
+};
+template <>
+struct DampLite<false> {
+  __device__ __forceinline__ void init(const Geo&, int, int) {}
+  __device__ __forceinline__ float upd(int, int, float C, float prev, float rhs) const {
+    return fmaf(2.0f, C, rhs) - prev;
+  }
+};
+#ifndef HV_BWD_LITE
+#define HV_BWD_LITE 0
+#endif
+template <bool SP>
+using BwdDamp = typename std::conditional<HV_BWD_LITE != 0, DampLite<SP>, Damp<SP>>::type;
 template <>
 struct Damp<false> {
   __device__ __forceinline__ void init(const Geo&, int, int) {}
@@ -171,9 +201,21 @@ struct Damp<false> {
 
 template <bool SP>
 __device__ __forceinline__ float dmp_ci(const Damp<SP>& d, int r, int i) {
-  if constexpr (SP) return d.ci[r][i];
+  if constexpr (SP) return d.ci(r, i);
   else return 1.0f;
 }
+
+// Consumer/producer bookkeeping of the NSTAGE-deep TMA ring (no divisions in the item loop).
+struct Ring {
+  int stage = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ void advance() {
+    if (++stage == NSTAGE) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+};
 
 template <bool SP>
 __device__ __forceinline__ void fwd_body(const CUtensorMap* mh, const CUtensorMap* mt, const CUtensorMap* mq,
@@ -184,139 +226,150 @@ __device__ __forceinline__ void fwd_body(const CUtensorMap* mh, const CUtensorMa
   const int grp = blockIdx.z;
   const int fb = grp * p.FG;
   const int nf = max(0, min(p.K, fb + p.FG) - fb);   // Born fields of this CTA
-  const int ips = 1 + nf;                             // items per shot: background, then its Born fields
-  const int nitems = p.S * ips;
+  const int nitems = p.S * (1 + nf);                  // per shot: background, then its Born fields
   const int par_n = p.n & 1, par_new = par_n ^ 1;
   const bool leader = (grp == 0) && p.bg_update;
   uint64_t* qbar = bars + NSTAGE;
-  // item inputs: halo of level n, tile of level n-1 (when this CTA updates the field)
-  auto issue = [&](int item) {
-    const int stage = item % NSTAGE;
-    const int s = item / ips, t = item % ips;
-    float* st = stages + stage * STAGE_FLOATS;
-    const bool upd = t > 0 || leader;
-    const int slot = t == 0 ? p.bg_slot : p.born_slot0 + fb + t - 1;
-    const int pl = (s * p.nslot + slot) * 2;
-    mbar_expect_tx(&bars[stage], TILE_BYTES + (upd ? PT_BYTES : 0));
-    tma_load_3d(st, mh, &bars[stage], x0 - R, z0 - R, pl + par_n);
-    if (upd) tma_load_3d(st + TILE_FLOATS, mt, &bars[stage], x0, z0, pl + par_new);
+
+  // producer (thread 0): next item (ps, pt) -> stage
+  int ps = 0, pt = 0, issued = 0;
+  Ring prod;
+  auto issue_next = [&]() {
+    float* st = stages + prod.stage * STAGE_FLOATS;
+    const bool upd = pt > 0 || leader;
+    const int slot = pt == 0 ? p.bg_slot : p.born_slot0 + fb + pt - 1;
+    const int pl = (ps * p.nslot + slot) * 2;
+    mbar_expect_tx(&bars[prod.stage], TILE_BYTES + (upd ? PT_BYTES : 0));
+    tma_load_3d(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_n);
+    if (upd) tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_new);
+    prod.advance();
+    if (++pt > nf) {
+      pt = 0;
+      ++ps;
+    }
+    ++issued;
   };
   if (tid == 0) {
     if (nf > 0) {  // q_k tiles of the group, once for all shots
       mbar_expect_tx(qbar, nf * PT_BYTES);
       for (int t = 0; t < nf; ++t) tma_load_3d(qs + t * PT_FLOATS, mq, qbar, x0, z0, fb + t);
     }
-    for (int i = 0; i < min(NSTAGE, nitems); ++i) issue(i);
+    while (issued < min(NSTAGE, nitems)) issue_next();
   }
 
   const int I0 = z0 + ty * RZ;
   const int J0 = x0 + tx * 4;
+  const int so = ty * RZ * TX + tx * 4;                       // smem offset of this thread's first point
+  const long long go = static_cast<long long>(I0) * g.P + J0;  // plane offset of this thread's first point
   float w[RZ][4];
 #pragma unroll
   for (int r = 0; r < RZ; ++r) {
-    const int I = min(I0 + r, g.Nz - 1);
-    const float4 wv = ldg4(p.W2 + static_cast<long long>(I) * g.P + J0);
+    const float4 wv = ldg4(p.W2 + static_cast<long long>(min(I0 + r, g.Nz - 1)) * g.P + J0);
     w[r][0] = wv.x, w[r][1] = wv.y, w[r][2] = wv.z, w[r][3] = wv.w;
   }
+  bool row_ok[RZ];
+#pragma unroll
+  for (int r = 0; r < RZ; ++r) row_ok[r] = !SP || I0 + r < g.Nz;
   Damp<SP> dmp;
   dmp.init(g, I0, J0);
   const int tile_id = blockIdx.y * g.ntx + blockIdx.x;
   const int rb = p.trec_beg[tile_id], re = p.trec_beg[tile_id + 1];
   const float amp = p.src_amp[p.n];
+  const long long data_stride = static_cast<long long>(g.nt) * g.nrec;
   if (nf > 0) mbar_wait(qbar, 0);
 
+  Ring cons;
+  auto release = [&]() {
+    __syncthreads();  // every thread is done with this stage
+    cons.advance();
+    if (tid == 0 && issued < nitems) {
+      fence_proxy_async();
+      issue_next();
+    }
+  };
+  auto sample = [&](const float* st, float* out) {  // d[n][r] = field^n[rec_r] from the staged tile
+    for (int q = rb + tid; q < re; q += NTHREADS) {
+      const int rid = p.trec_id[q];
+      const int lz = p.rec_I[rid] - z0 + R, lx = p.rec_J[rid] - x0 + R;
+      out[static_cast<long long>(p.n) * g.nrec + rid] = st[lz * HX + lx];
+    }
+  };
+  auto store_row = [&](float* dst, int r, float (&v)[4]) {
+    if (SP) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (J0 + i >= g.Nx) v[i] = 0.0f;
+    }
+    if (row_ok[r]) st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
+  };
+
   float Lb[RZ][4];
-  int sI = -1, sJ = -1;
-  for (int item = 0; item < nitems; ++item) {
-    const int stage = item % NSTAGE;
-    const int s = item / ips, t = item % ips;
-    const float* st = stages + stage * STAGE_FLOATS;
-    const int slot = t == 0 ? p.bg_slot : p.born_slot0 + fb + t - 1;
-    const bool upd = t > 0 || leader;
-    if (t == 0) {
-      sI = p.src_I[p.shot0 + s];
-      sJ = p.src_J[p.shot0 + s];
-    }
-    mbar_wait(&bars[stage], (item / NSTAGE) & 1);
-    float L[RZ][4], C[RZ][4];
-    lap_points(st, tx, ty, L, C);
-    if (t == 0) {
-#pragma unroll
-      for (int r = 0; r < RZ; ++r)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) Lb[r][i] = L[r][i];
-    }
-    if (upd) {
-      float* __restrict__ dst = p.pool + (static_cast<long long>(s * p.nslot + slot) * 2 + par_new) * g.plane;
-      const float* qk = qs + (t > 0 ? t - 1 : 0) * PT_FLOATS;
-#pragma unroll
-      for (int r = 0; r < RZ; ++r) {
-        const int I = I0 + r;
-        const int o = (ty * RZ + r) * TX + tx * 4;
-        const float4 pv = ld4(st + TILE_FLOATS + o);
-        float4 qv = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (t > 0) qv = ld4(qk + o);
-        float v[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float rhs = w[r][i] * L[r][i];
-          if (t > 0) rhs = fmaf(f4(qv, i), Lb[r][i], rhs);
-          v[i] = dmp.upd(r, i, C[r][i], f4(pv, i), rhs);
-        }
-        if (t == 0 && I == sI && sJ >= J0 && sJ < J0 + 4) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (J0 + i == sJ) v[i] += amp * dmp_ci(dmp, r, i);
-        }
-        if (SP) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (J0 + i >= g.Nx) v[i] = 0.0f;
-          if (I >= g.Nz) continue;
-        }
-        st4(dst + static_cast<long long>(I) * g.P + J0, make_float4(v[0], v[1], v[2], v[3]));
-      }
-    }
-    // imaging-factor store s^n = 2 dt^2 / (v h^2) * L~u^n on the interior (FULL store / replay segments)
-    if (t == 0 && leader && p.s_out != nullptr) {
-      const int jc = J0 - g.c0;
-      if (jc >= 0 && jc < g.PI) {
+  for (int s = 0; s < p.S; ++s) {
+    // ---------------- background u of shot s: L u^n (kept for the Born sources), leader updates u
+    {
+      const float* st = stages + cons.stage * STAGE_FLOATS;
+      mbar_wait(&bars[cons.stage], cons.phase);
+      float C[RZ][4];
+      lap_points(st, tx, ty, Lb, C);
+      if (leader) {
+        float* dst = p.pool + (static_cast<long long>(s * p.nslot + p.bg_slot) * 2 + par_new) * g.plane;
+        const int sI = p.src_I[p.shot0 + s], sJ = p.src_J[p.shot0 + s];
 #pragma unroll
         for (int r = 0; r < RZ; ++r) {
-          const int iz = I0 + r - g.W;
-          if (iz < 0 || iz >= g.nz) continue;
-          const float4 ic = ldg4(p.imgc + static_cast<long long>(iz) * g.PI + jc);
-          float o[4];
+          const float4 pv = ld4(st + TILE_FLOATS + so + r * TX);
+          float v[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int ix = J0 + i - g.W;
-            o[i] = (!SP || (ix >= 0 && ix < g.nx)) ? f4(ic, i) * Lb[r][i] : 0.0f;
+          for (int i = 0; i < 4; ++i) v[i] = dmp.upd(r, i, C[r][i], f4(pv, i), w[r][i] * Lb[r][i]);
+          if (I0 + r == sI && sJ >= J0 && sJ < J0 + 4) {  // point source dt^2 s[n] / h^2 (/(1 + c))
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (J0 + i == sJ) v[i] += amp * dmp_ci(dmp, r, i);
           }
-          st4(p.s_out + s * p.s_shot_stride + static_cast<long long>(iz) * g.PI + jc,
-              make_float4(o[0], o[1], o[2], o[3]));
+          store_row(dst, r, v);
         }
-      }
-    }
-    // receiver sampling of level n from the staged tile (d[n] = u^n[rec]; level nt-1 by gather_last_kernel)
-    if (re > rb) {
-      float* out = nullptr;
-      if (t == 0) {
-        if (leader && p.d_bg) out = p.d_bg + static_cast<long long>(p.dbg_shot0 + s) * g.nt * g.nrec;
-      } else if (p.d_born) {
-        out = p.d_born + (static_cast<long long>(s) * p.K + (fb + t - 1)) * g.nt * g.nrec;
-      }
-      if (out) {
-        for (int q = rb + tid; q < re; q += NTHREADS) {
-          const int rid = p.trec_id[q];
-          const int lz = p.rec_I[rid] - z0 + R, lx = p.rec_J[rid] - x0 + R;
-          out[static_cast<long long>(p.n) * g.nrec + rid] = st[lz * HX + lx];
+        // imaging-factor store s^n = 2 dt^2 / (v h^2) * L~u^n on the interior (FULL store / replay segments)
+        const int jc = J0 - g.c0;
+        if (p.s_out != nullptr && jc >= 0 && jc < g.PI) {
+#pragma unroll
+          for (int r = 0; r < RZ; ++r) {
+            const int iz = I0 + r - g.W;
+            if (iz < 0 || iz >= g.nz) continue;
+            const float4 ic = ldg4(p.imgc + static_cast<long long>(iz) * g.PI + jc);
+            float o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int ix = J0 + i - g.W;
+              o[i] = (!SP || (ix >= 0 && ix < g.nx)) ? f4(ic, i) * Lb[r][i] : 0.0f;
+            }
+            st4(p.s_out + s * p.s_shot_stride + static_cast<long long>(iz) * g.PI + jc,
+                make_float4(o[0], o[1], o[2], o[3]));
+          }
         }
+        if (re > rb && p.d_bg) sample(st, p.d_bg + (p.dbg_shot0 + s) * data_stride);
       }
+      release();
     }
-    __syncthreads();  // every thread is done with this stage
-    if (tid == 0 && item + NSTAGE < nitems) {
-      fence_proxy_async();
-      issue(item + NSTAGE);
+    // ---------------- Born fields du_k of shot s: source q_k L u^n
+    float* born_base = p.pool + (static_cast<long long>(s * p.nslot + p.born_slot0 + fb) * 2 + par_new) * g.plane;
+    for (int t = 0; t < nf; ++t) {
+      const float* st = stages + cons.stage * STAGE_FLOATS;
+      mbar_wait(&bars[cons.stage], cons.phase);
+      float L[RZ][4], C[RZ][4];
+      lap_points(st, tx, ty, L, C);
+      float* dst = born_base + static_cast<long long>(t) * 2 * g.plane;
+      const float* qk = qs + t * PT_FLOATS + so;
+#pragma unroll
+      for (int r = 0; r < RZ; ++r) {
+        const float4 pv = ld4(st + TILE_FLOATS + so + r * TX);
+        const float4 qv = ld4(qk + r * TX);
+        float v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          v[i] = dmp.upd(r, i, C[r][i], f4(pv, i), fmaf(f4(qv, i), Lb[r][i], w[r][i] * L[r][i]));
+        store_row(dst, r, v);
+      }
+      if (re > rb && p.d_born) sample(st, p.d_born + (static_cast<long long>(s) * p.K + fb + t) * data_stride);
+      release();
     }
   }
 }
@@ -378,23 +431,31 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   if (nf <= 0) return;
   const int nitems = p.S * nf;
   const int par_in = (p.j + 1) & 1, par_out = p.j & 1;
-  auto issue = [&](int item) {
-    const int stage = item % NSTAGE;
-    const int s = item / nf, t = item % nf;
-    float* st = stages + stage * STAGE_FLOATS;
-    const int pl = (s * p.nslot + p.slot0 + fb + t) * 2;
-    mbar_expect_tx(&bars[stage], TILE_BYTES + (p.update ? PT_BYTES : 0));
-    tma_load_3d(st, mh, &bars[stage], x0 - R, z0 - R, pl + par_in);
-    if (p.update) tma_load_3d(st + TILE_FLOATS, mt, &bars[stage], x0, z0, pl + par_out);
+  int ps = 0, pt = 0, issued = 0;
+  Ring prod;
+  auto issue_next = [&]() {
+    float* st = stages + prod.stage * STAGE_FLOATS;
+    const int pl = (ps * p.nslot + p.slot0 + fb + pt) * 2;
+    mbar_expect_tx(&bars[prod.stage], TILE_BYTES + (p.update ? PT_BYTES : 0));
+    tma_load_3d(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_in);
+    if (p.update) tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_out);
+    prod.advance();
+    if (++pt == nf) {
+      pt = 0;
+      ++ps;
+    }
+    ++issued;
   };
   if (tid == 0) {
-    for (int i = 0; i < min(NSTAGE, nitems); ++i) issue(i);
+    while (issued < min(NSTAGE, nitems)) issue_next();
   }
   const int I0 = z0 + ty * RZ;
   const int J0 = x0 + tx * 4;
+  const int so = ty * RZ * TX + tx * 4;
+  const long long go = static_cast<long long>(I0) * g.P + J0;
   const int jc = J0 - g.c0;
   float w[RZ][4];
-  bool img_rows[RZ];
+  bool img_rows[RZ], row_ok[RZ];
   bool any_img = false;
 #pragma unroll
   for (int r = 0; r < RZ; ++r) {
@@ -405,6 +466,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
     img_rows[r] = p.imaging && iz >= 0 && iz < g.nz && J0 + 3 >= g.W && J0 < g.W + g.nx && jc >= 0 &&
                   jc < g.PI;
     any_img |= img_rows[r];
+    row_ok[r] = !SP || I < g.Nz;
   }
   // imaging factor s^j of shot s for this thread's points (prefetched one shot ahead)
   auto load_sj = [&](int s, float4 (&dst)[RZ]) {
@@ -417,10 +479,11 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   };
   float4 snext[RZ];
   load_sj(0, snext);
-  Damp<SP> dmp;
+  BwdDamp<SP> dmp;
   dmp.init(g, I0, J0);
   const int tile_id = blockIdx.y * g.ntx + blockIdx.x;
   const int rb = p.trec_beg[tile_id], re = p.trec_beg[tile_id + 1];
+  const long long data_stride = static_cast<long long>(g.nt) * g.nrec;
   float acc[BWD_FG][RZ][4];
 #pragma unroll
   for (int t = 0; t < BWD_FG; ++t)
@@ -429,6 +492,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[t][r][i] = 0.0f;
 
+  Ring cons;
   for (int s = 0; s < p.S; ++s) {
     float sj[RZ][4];
 #pragma unroll
@@ -440,22 +504,19 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
       }
     }
     if (any_img && s + 1 < p.S) load_sj(s + 1, snext);
+    float* out_base = p.pool + (static_cast<long long>(s * p.nslot + p.slot0 + fb) * 2 + par_out) * g.plane;
 #pragma unroll
     for (int t = 0; t < BWD_FG; ++t) {
       if (t >= nf) break;
-      const int item = s * nf + t;
-      const int stage = item % NSTAGE;
-      const float* st = stages + stage * STAGE_FLOATS;
-      const int slot = p.slot0 + fb + t;
-      float* __restrict__ dst = p.pool + (static_cast<long long>(s * p.nslot + slot) * 2 + par_out) * g.plane;
-      mbar_wait(&bars[stage], (item / NSTAGE) & 1);
+      const float* st = stages + cons.stage * STAGE_FLOATS;
+      float* dst = out_base + static_cast<long long>(t) * 2 * g.plane;
+      mbar_wait(&bars[cons.stage], cons.phase);
       float L[RZ][4], C[RZ][4];
       lap_points(st, tx, ty, L, C);
       if (p.update) {
 #pragma unroll
         for (int r = 0; r < RZ; ++r) {
-          const int I = I0 + r;
-          const float4 pv = ld4(st + TILE_FLOATS + (ty * RZ + r) * TX + tx * 4);
+          const float4 pv = ld4(st + TILE_FLOATS + so + r * TX);
           float v[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) v[i] = dmp.upd(r, i, C[r][i], f4(pv, i), w[r][i] * L[r][i]);
@@ -463,9 +524,8 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
 #pragma unroll
             for (int i = 0; i < 4; ++i)
               if (J0 + i >= g.Nx) v[i] = 0.0f;
-            if (I >= g.Nz) continue;
           }
-          st4(dst + static_cast<long long>(I) * g.P + J0, make_float4(v[0], v[1], v[2], v[3]));
+          if (row_ok[r]) st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
         }
       }
       // zero-lag imaging, summed over the batch's shots in registers: acc += s^j * lambda^{j+1}
@@ -474,15 +534,16 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[t][r][i] = fmaf(sj[r][i], C[r][i], acc[t][r][i]);
       __syncthreads();  // stage consumed and lambda^j of this tile stored
-      if (tid == 0 && item + NSTAGE < nitems) {
+      cons.advance();
+      if (tid == 0 && issued < nitems) {
         fence_proxy_async();
-        issue(item + NSTAGE);
+        issue_next();
       }
       // receiver injection into lambda^j: += v^2 / (1 + c) * rho[j][r]   (R^T scatter-add)
       if (p.update && re > rb) {
-        const float* rho = (slot == 0)
-                               ? p.rho_res + static_cast<long long>(s) * g.nt * g.nrec
-                               : p.rho_born + (static_cast<long long>(s) * p.Kb + (slot - 1)) * g.nt * g.nrec;
+        const int slot = p.slot0 + fb + t;
+        const float* rho = (slot == 0) ? p.rho_res + s * data_stride
+                                       : p.rho_born + (static_cast<long long>(s) * p.Kb + (slot - 1)) * data_stride;
         for (int q = rb + tid; q < re; q += NTHREADS) {
           const int rid = p.trec_id[q];
           const float val = p.rec_coef[rid] * rho[static_cast<long long>(p.j) * g.nrec + rid];
@@ -495,11 +556,11 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
 #pragma unroll
     for (int t = 0; t < BWD_FG; ++t) {
       if (t >= nf) break;
-      float* a = p.acc + static_cast<long long>(p.slot0 + fb + t) * g.plane;
+      float* a = p.acc + static_cast<long long>(p.slot0 + fb + t) * g.plane + go;
 #pragma unroll
       for (int r = 0; r < RZ; ++r) {
         if (!img_rows[r]) continue;
-        atomicAdd(reinterpret_cast<float4*>(a + static_cast<long long>(I0 + r) * g.P + J0),
+        atomicAdd(reinterpret_cast<float4*>(a + static_cast<long long>(r) * g.P),
                   make_float4(acc[t][r][0], acc[t][r][1], acc[t][r][2], acc[t][r][3]));
       }
     }

@@ -245,3 +245,45 @@ def test_psido_apply_parity(hv, nz, nx, r):
         out = s.psido_apply(a, b, v, mode)
         ref = opsido.apply_mode(a.astype(np.float64), b.astype(np.complex128), v.astype(np.float64), mode)
         assert rel_l2(out, ref) <= TOL, (mode, rel_l2(out, ref))
+
+
+# ---------------------------------------------------------------------------------------------- cfg 2 / 3 / 4
+# Full BASELINE grids in their launch configurations, against the oracle on the SURVEY.md §8(d) parity
+# sub-slices. The time axis is truncated (the fp64 numpy oracle needs ~18 ms per field-step on the 424 x 1192
+# cfg 2 grid and ~0.45 s on the 2088 x 6184 cfg 4 grid); the full-length runs are covered by the properties above.
+
+
+@pytest.mark.parametrize("store", ["full", "checkpoint"])
+def test_cfg2_full_grid_fused_gradient_hessvec_slice(hv, store):
+    wl = W.config(2).subset(shots=[31], nt=300)
+    V = wl.probes([0, 1])
+    pb = wave.Problem(wl)
+    d_obs = wave.Problem(wl, wl.model_true).forward_all().astype(np.float32)
+    phi, g = pb.gradient(d_obs, mode="checkpoint", ckpt=17)
+    HV = pb.hessvec(list(V.astype(np.float64)), mode="checkpoint", ckpt=17)
+    s = hv.Solver.from_workload(wl, store=store)
+    phig, gg, hvg = s.gradient_hessvec(wl.model, d_obs, V)
+    assert rel_l2(gg, g) <= TOL, rel_l2(gg, g)
+    assert rel_l2(hvg, HV) <= TOL, rel_l2(hvg, HV)
+    assert abs(phig - phi) <= TOL * phi
+
+
+def test_cfg3_full_grid_pdo_probe_slice(hv):
+    """Rademacher probe k = 0 and cosine probe k = 16 (kappa = (1/16, 1/16), in band), shot 31."""
+    wl = W.config(3).subset(shots=[31], nt=300)
+    V = wl.probes([0, 16])
+    ref = wave.Problem(wl).hessvec(list(V.astype(np.float64)), mode="checkpoint", ckpt=17)
+    out = hv.Solver.from_workload(wl).hessvec(wl.model, V)
+    for k in range(2):
+        assert rel_l2(out[k], ref[k]) <= TOL, (k, rel_l2(out[k], ref[k]))
+
+
+def test_cfg4_full_grid_checkpoint_slice(hv):
+    """2048 x 6144 (12.9 M padded points) in CHECKPOINT mode: shot 127, probe 0, nt truncated to 100."""
+    wl = W.config(4).subset(shots=[127], nt=100)
+    V = wl.probes([0])
+    ref = wave.Problem(wl).hessvec(list(V.astype(np.float64)), mode="checkpoint", ckpt=10)
+    s = hv.Solver.from_workload(wl, store="checkpoint", ckpt_interval=9)
+    out = s.hessvec(wl.model, V)
+    assert s.stats()["store"] == 2
+    assert rel_l2(out, ref) <= TOL, rel_l2(out, ref)

@@ -55,6 +55,8 @@ extern "C" {
 #define HV_STORE_AUTO       0  /* FULL when it fits the budget, else CHECKPOINT                      */
 #define HV_STORE_FULL       1  /* keep the imaging factor (2 dt^2 / v) L u^n of every level in HBM    */
 #define HV_STORE_CHECKPOINT 2  /* keep (u^n, u^{n-1}) every ckpt_interval levels, replay segments      */
+#define HV_STORE_BOUNDARY   3  /* keep the 4-cell ring around the interior of every level; rebuild the
+                                  background backwards (time-reversed leapfrog on the interior)          */
 
 typedef struct hv_ctx hv_ctx;
 
@@ -71,7 +73,7 @@ typedef struct {
   const int32_t *rec_iz, *rec_ix;
   const float *wavelet;  /* HOST [nt]: source function s[n] (copied)                                     */
   int32_t src_begin, src_end; /* this rank's shot shard [begin, end); end = 0 means nsrc                  */
-  int32_t store;         /* HV_STORE_*                                                                   */
+  int32_t store;         /* HV_STORE_* (AUTO: FULL if it fits, else CHECKPOINT)                         */
   int32_t ckpt_interval; /* CHECKPOINT spacing in levels; 0 = round(sqrt(nt))                            */
   int32_t shot_batch;    /* shots propagated concurrently; 0 = auto from the memory budget               */
   int32_t field_group;   /* Born / adjoint fields per CTA (tuning); 0 = auto                               */

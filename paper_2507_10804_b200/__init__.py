@@ -25,7 +25,7 @@ LIB_PATH = os.environ.get("HV_LIB") or os.path.join(_HERE, "libhv.so")  # HV_LIB
 
 HV_OK, HV_EINVAL, HV_EGRID, HV_ECFL, HV_ENOMEM, HV_ECUDA, HV_ESTATE = range(7)
 STATUS = {0: "HV_OK", 1: "HV_EINVAL", 2: "HV_EGRID", 3: "HV_ECFL", 4: "HV_ENOMEM", 5: "HV_ECUDA", 6: "HV_ESTATE"}
-STORE = {"auto": 0, "full": 1, "checkpoint": 2}
+STORE = {"auto": 0, "full": 1, "checkpoint": 2, "boundary": 3}
 
 
 class HVError(RuntimeError):

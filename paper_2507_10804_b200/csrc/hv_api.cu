@@ -83,6 +83,7 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
     if (grad) b += F4 * 2.0 * g.nt * g.nrec;                                    // data + residual
     if (adjoint) {
       if (store == HV_STORE_FULL) b += F4 * (double)g.nt * g.iplane;
+      else if (store == HV_STORE_BOUNDARY) b += F4 * ((double)g.nt * ring_size(g) + 2.0 * g.iplane);
       else b += F4 * (2.0 * ((g.nt - 1 + k - 1) / k) * g.plane + (double)k * g.iplane);
     }
     return b;
@@ -93,7 +94,7 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
   if (!adjoint) store = HV_STORE_FULL;  // forward only: nothing stored
   if (store == HV_STORE_AUTO) store = (shared + per_shot(HV_STORE_FULL, k) <= budget) ? HV_STORE_FULL
                                                                                        : HV_STORE_CHECKPOINT;
-  if (store != HV_STORE_FULL && store != HV_STORE_CHECKPOINT)
+  if (store != HV_STORE_FULL && store != HV_STORE_CHECKPOINT && store != HV_STORE_BOUNDARY)
     return fail(c, HV_EINVAL, "unknown storage mode " + std::to_string(store));
   pl->store = store;
   pl->k = k;
@@ -193,7 +194,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
 
   // --- workspace
   float *pool, *dborn = nullptr, *dbg = nullptr, *rres = nullptr, *acc = nullptr, *store = nullptr,
-               *ckpt = nullptr, *seg = nullptr;
+               *ckpt = nullptr, *seg = nullptr, *ring = nullptr, *sbuf = nullptr;
+  const long long ringN = ring_size(g);
   const long long planes_per_shot = 2LL * nslot;
   if ((st = ws_get(c, "pool", sizeof(float) * g.plane * planes_per_shot * S, (void**)&pool))) return st;
   if (K > 0 && (st = ws_get(c, "dborn", sizeof(float) * (size_t)S * K * g.nt * g.nrec, (void**)&dborn))) return st;
@@ -206,6 +208,9 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     CU_TRY(cudaMemsetAsync(acc, 0, sizeof(float) * g.plane * pl.nacc, c->stream));
     if (pl.store == HV_STORE_FULL) {
       if ((st = ws_get(c, "store", sizeof(float) * g.iplane * g.nt * S, (void**)&store))) return st;
+    } else if (pl.store == HV_STORE_BOUNDARY) {
+      if ((st = ws_get(c, "ring", sizeof(float) * ringN * g.nt * S, (void**)&ring))) return st;
+      if ((st = ws_get(c, "sbuf", sizeof(float) * g.iplane * 2 * S, (void**)&sbuf))) return st;
     } else {
       if ((st = ws_get(c, "ckpt", sizeof(float) * g.plane * 2 * pl.nck * S, (void**)&ckpt))) return st;
       if ((st = ws_get(c, "seg", sizeof(float) * g.iplane * pl.k * S, (void**)&seg))) return st;
@@ -271,7 +276,10 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
       fp.dbg_shot0 = 0;
     }
     const bool full = adjoint && pl.store == HV_STORE_FULL;
+    const bool boundary = adjoint && pl.store == HV_STORE_BOUNDARY;
     fp.s_shot_stride = full ? g.iplane * g.nt : 0;
+    fp.ring_shot_stride = ringN * g.nt;
+    if (boundary) CU_TRY(cudaMemsetAsync(ring, 0, sizeof(float) * ringN * g.nt * Sb, c->stream));
     const dim3 gridf(g.ntx, g.ntz, Gf);
     for (int n = 0; n <= g.nt - 2; ++n) {
       if (adjoint && pl.store == HV_STORE_CHECKPOINT && n % pl.k == 0) {
@@ -283,6 +291,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
       }
       fp.n = n;
       fp.s_out = full ? store + (size_t)n * g.iplane : nullptr;
+      fp.ring_out = boundary ? ring + (size_t)(n + 1) * ringN : nullptr;
       fwd_step_kernel<<<gridf, block, fwd_smem, c->stream>>>(map_halo, map_tile, map_q, fp);
       launches++;
     }
@@ -301,7 +310,16 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
                                                               phi_d);
         launches++;
       }
-      CU_TRY(cudaMemsetAsync(pool, 0, sizeof(float) * g.plane * planes_per_shot * Sb, c->stream));
+      if (boundary) {  // keep u^{nt-1}, u^{nt-2} (slot 0) in the replay slot; clear the adjoint slots
+        for (int s = 0; s < Sb; ++s) {
+          float* base = pool + (size_t)s * planes_per_shot * g.plane;
+          CU_TRY(cudaMemcpyAsync(base + (size_t)replay_slot * 2 * g.plane, base, sizeof(float) * 2 * g.plane,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+          CU_TRY(cudaMemsetAsync(base, 0, sizeof(float) * g.plane * 2 * replay_slot, c->stream));
+        }
+      } else {
+        CU_TRY(cudaMemsetAsync(pool, 0, sizeof(float) * g.plane * planes_per_shot * Sb, c->stream));
+      }
       BwdParams bp{};
       bp.g = g;
       bp.pool = pool;
@@ -327,7 +345,29 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
         bp.update = j >= 2;
         bp.imaging = j <= g.nt - 2;
         if (bp.imaging) {
-          if (full) {
+          if (boundary) {  // a6: rebuild u^{j-1} and emit s^j
+            RevParams rv{};
+            rv.g = g;
+            rv.nslot = nslot;
+            rv.pool = pool;
+            rv.slot = replay_slot;
+            rv.j = j;
+            rv.S = Sb;
+            rv.shot0 = b0;
+            rv.W2 = W2;
+            rv.imgc = imgc;
+            rv.s_out = sbuf + (size_t)(j & 1) * Sb * g.iplane;
+            rv.s_shot_stride = g.iplane;
+            rv.ring_in = ring + (size_t)(j - 1) * ringN;
+            rv.ring_shot_stride = ringN * g.nt;
+            rv.src_I = c->d_srcI;
+            rv.src_J = c->d_srcJ;
+            rv.src_amp = c->d_src_amp;
+            rev_step_kernel<<<dim3(g.ntx, g.ntz, 1), block, BWD_SMEM_BYTES, c->stream>>>(map_halo, map_tile, rv);
+            launches++;
+            bp.s_lvl = rv.s_out;
+            bp.s_shot_stride = g.iplane;
+          } else if (full) {
             bp.s_lvl = store + (size_t)j * g.iplane;
             bp.s_shot_stride = g.iplane * g.nt;
           } else {
@@ -536,6 +576,8 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
                            fwd_smem_bytes(FWD_FG_MAX)) !=
           cudaSuccess ||
       cudaFuncSetAttribute(bwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_BYTES) !=
+          cudaSuccess ||
+      cudaFuncSetAttribute(rev_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_BYTES) !=
           cudaSuccess) {
     cudaGetLastError();
     hv_destroy(c);

@@ -114,6 +114,20 @@ __device__ __forceinline__ bool tile_is_interior(const Geo& g, int x0, int z0) {
   return z0 >= g.W && z0 + TZ <= g.W + g.nz && x0 >= g.W && x0 + TX <= g.W + g.nx;
 }
 
+// BOUNDARY store: index of padded cell (I, J) in the RING-cell band around the interior, or -1.
+// Layout: top band [R][nx + 2R], bottom band [R][nx + 2R], left band [nz][R], right band [nz][R].
+__device__ __forceinline__ int ring_index(const Geo& g, int I, int J) {
+  const int zi = I - (g.W - R), xi = J - (g.W - R);
+  const int wz = g.nz + 2 * R, wx = g.nx + 2 * R;
+  if (zi < 0 || zi >= wz || xi < 0 || xi >= wx) return -1;
+  if (zi < R) return zi * wx + xi;
+  if (zi >= R + g.nz) return R * wx + (zi - R - g.nz) * wx + xi;
+  if (xi < R) return 2 * R * wx + (zi - R) * R + xi;
+  if (xi >= R + g.nx) return 2 * R * wx + g.nz * R + (zi - R) * R + (xi - R - g.nx);
+  return -1;  // interior
+}
+__host__ __device__ __forceinline__ int ring_size(const Geo& g) { return 2 * R * (g.nx + 2 * R) + 2 * R * g.nz; }
+
 // ------------------------------------------------------------------------------------------------ forward
 
 struct FwdParams {
@@ -142,6 +156,8 @@ struct FwdParams {
   float* d_bg;            // background data [..][nt][nrec], row dbg_shot0 + s_local, or null
   int dbg_shot0;
   float* d_born;          // [S][K][nt][nrec] Born data (batch-local) or null
+  float* ring_out;        // BOUNDARY store: ring of u^{n+1} for batch shot 0, or null
+  long long ring_shot_stride;
 };
 
 // Per-point damping of this thread's points (SP: the tile touches the sponge): (1 - c) and 1 / (1 + c).
@@ -324,6 +340,13 @@ __device__ __forceinline__ void fwd_body(const CUtensorMap* mh, const CUtensorMa
 #pragma unroll
             for (int i = 0; i < 4; ++i)
               if (J0 + i == sJ) v[i] += amp * dmp_ci(dmp, r, i);
+          }
+          if (SP && p.ring_out != nullptr) {  // BOUNDARY store: the ring of u^{n+1}
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int q = ring_index(g, I0 + r, J0 + i);
+              if (q >= 0) p.ring_out[s * p.ring_shot_stride + q] = v[i];
+            }
           }
           store_row(dst, r, v);
         }
@@ -584,6 +607,137 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     bwd_body<false>(&mh, &mt, p, stages, bars);
   else
     bwd_body<true>(&mh, &mt, p, stages, bars);
+}
+
+// ------------------------------------------------------------------------------------------------ reverse (a6)
+
+// BOUNDARY mode: rebuild the background backwards, u^{j-1} = 2 u^j - u^{j+1} + w L u^j + dt^2 f^j on the interior
+// (c = 0 there) and the stored ring elsewhere in the Laplacian's reach, and emit s^j = 2 dt^2 / (v h^2) L~u^j.
+struct RevParams {
+  Geo g;
+  int nslot;
+  float* pool;
+  int slot;               // background replay slot
+  int j;                  // level whose Laplacian is taken; writes level j-1 in place over level j+1
+  int S;
+  int shot0;
+  const float* W2;
+  const float* imgc;
+  float* s_out;           // s^j for batch shot 0 ([nz][PI] per shot)
+  long long s_shot_stride;
+  const float* ring_in;   // ring of level j-1 for batch shot 0
+  long long ring_shot_stride;
+  const int* src_I;
+  const int* src_J;
+  const float* src_amp;
+};
+
+template <bool SP>
+__device__ __forceinline__ void rev_body(const CUtensorMap* mh, const CUtensorMap* mt, const RevParams& p,
+                                         float* stages, uint64_t* bars) {
+  const Geo& g = p.g;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
+  const int x0 = blockIdx.x * TX, z0 = blockIdx.y * TZ;
+  const int par_j = p.j & 1, par_o = par_j ^ 1;
+  int issued = 0;
+  Ring prod;
+  auto issue_next = [&]() {
+    float* st = stages + prod.stage * STAGE_FLOATS;
+    const int pl = (issued * p.nslot + p.slot) * 2;
+    mbar_expect_tx(&bars[prod.stage], TILE_BYTES + PT_BYTES);
+    tma_load_3d(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_j);
+    tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_o);
+    prod.advance();
+    ++issued;
+  };
+  if (tid == 0) {
+    while (issued < min(NSTAGE, p.S)) issue_next();
+  }
+  const int I0 = z0 + ty * RZ;
+  const int J0 = x0 + tx * 4;
+  const int so = ty * RZ * TX + tx * 4;
+  const long long go = static_cast<long long>(I0) * g.P + J0;
+  float w[RZ][4];
+  int rq[RZ][4];       // ring index (>= 0), interior (-1), or neither (-2)
+#pragma unroll
+  for (int r = 0; r < RZ; ++r) {
+    const float4 wv = ldg4(p.W2 + static_cast<long long>(min(I0 + r, g.Nz - 1)) * g.P + J0);
+    w[r][0] = wv.x, w[r][1] = wv.y, w[r][2] = wv.z, w[r][3] = wv.w;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int I = I0 + r, J = J0 + i;
+      const bool in = I >= g.W && I < g.W + g.nz && J >= g.W && J < g.W + g.nx;
+      rq[r][i] = SP ? (in ? -1 : (ring_index(g, I, J) >= 0 ? ring_index(g, I, J) : -2)) : -1;
+    }
+  }
+  const float amp = p.src_amp[p.j];
+  const int jc = J0 - g.c0;
+  Ring cons;
+  for (int s = 0; s < p.S; ++s) {
+    const float* st = stages + cons.stage * STAGE_FLOATS;
+    mbar_wait(&bars[cons.stage], cons.phase);
+    float L[RZ][4], C[RZ][4];
+    lap_points(st, tx, ty, L, C);
+    float* dst = p.pool + (static_cast<long long>(s * p.nslot + p.slot) * 2 + par_o) * g.plane;
+    const int sI = p.src_I[p.shot0 + s], sJ = p.src_J[p.shot0 + s];
+#pragma unroll
+    for (int r = 0; r < RZ; ++r) {
+      const float4 nx1 = ld4(st + TILE_FLOATS + so + r * TX);  // u^{j+1}
+      float v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        v[i] = fmaf(2.0f, C[r][i], fmaf(w[r][i], L[r][i], -f4(nx1, i)));
+        if (I0 + r == sI && J0 + i == sJ) v[i] += amp;
+        if (SP && rq[r][i] >= 0) v[i] = p.ring_in[s * p.ring_shot_stride + rq[r][i]];
+      }
+      if (!SP) {
+        st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
+      } else if (I0 + r < g.Nz) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (rq[r][i] != -2) dst[go + static_cast<long long>(r) * g.P + i] = v[i];
+      }
+      // s^j on the interior
+      const int iz = I0 + r - g.W;
+      if (iz >= 0 && iz < g.nz && jc >= 0 && jc < g.PI) {
+        const float4 ic = ldg4(p.imgc + static_cast<long long>(iz) * g.PI + jc);
+        float o[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] = (!SP || rq[r][i] == -1) ? f4(ic, i) * L[r][i] : 0.0f;
+        st4(p.s_out + s * p.s_shot_stride + static_cast<long long>(iz) * g.PI + jc,
+            make_float4(o[0], o[1], o[2], o[3]));
+      }
+    }
+    __syncthreads();
+    cons.advance();
+    if (tid == 0 && issued < p.S) {
+      fence_proxy_async();
+      issue_next();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NTHREADS, 2)
+    rev_step_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
+                    const RevParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stages = reinterpret_cast<float*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES_BYTES);
+  const int x0 = blockIdx.x * TX, z0 = blockIdx.y * TZ;
+  const Geo& g = p.g;
+  // tiles entirely outside interior + ring have nothing to rebuild
+  if (z0 + TZ <= g.W - R || z0 >= g.W + g.nz + R || x0 + TX <= g.W - R || x0 >= g.W + g.nx + R) return;
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    tma_prefetch_desc(&mh);
+    tma_prefetch_desc(&mt);
+    for (int i = 0; i < NSTAGE; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tile_is_interior(g, x0, z0))
+    rev_body<false>(&mh, &mt, p, stages, bars);
+  else
+    rev_body<true>(&mh, &mt, p, stages, bars);
 }
 
 // ------------------------------------------------------------------------------------------------ helpers

@@ -53,13 +53,13 @@ def test_cfg0_forward(hv, cfg0_ref):
     assert rel_l2(dg, d) <= TOL, rel_l2(dg, d)
 
 
-@pytest.mark.parametrize("store", ["full", "checkpoint"])
+@pytest.mark.parametrize("store", ["full", "checkpoint", "boundary"])
 def test_cfg0_hessvec(hv, cfg0_ref, store):
     wl, V, d, HV, *_ = cfg0_ref
     s = hv.Solver.from_workload(wl, store=store)
     out = s.hessvec(wl.model, V)
     assert rel_l2(out, HV) <= TOL, rel_l2(out, HV)
-    assert s.stats()["store"] == (1 if store == "full" else 2)
+    assert s.stats()["store"] == hv.STORE[store]
 
 
 def test_cfg0_gradient(hv, cfg0_ref):
@@ -118,6 +118,7 @@ def ragged():
 @pytest.mark.parametrize("store,ckpt,batch,fg", [
     ("full", 0, 1, 8), ("full", 0, 2, 1), ("full", 0, 3, 2),
     ("checkpoint", 7, 1, 8), ("checkpoint", 0, 3, 1), ("checkpoint", 299, 2, 3),
+    ("boundary", 0, 1, 8), ("boundary", 0, 3, 2),
 ])
 def test_ragged_hessvec_modes(hv, ragged, store, ckpt, batch, fg):
     wl, V, d, HV, *_ = ragged
@@ -128,9 +129,10 @@ def test_ragged_hessvec_modes(hv, ragged, store, ckpt, batch, fg):
         assert rel_l2(out[k], HV[k]) <= TOL
 
 
-def test_ragged_forward_gradient(hv, ragged):
+@pytest.mark.parametrize("store", ["full", "checkpoint", "boundary"])
+def test_ragged_forward_gradient(hv, ragged, store):
     wl, V, d, HV, d_obs, phi, g, m_start = ragged
-    s = hv.Solver.from_workload(wl, shot_batch=2)
+    s = hv.Solver.from_workload(wl, shot_batch=2, store=store)
     assert rel_l2(s.forward(wl.model), d) <= TOL
     phig, gg = s.gradient(m_start, d_obs)
     assert rel_l2(gg, g) <= TOL and abs(phig - phi) <= TOL * phi
@@ -227,6 +229,10 @@ def test_cfg1_full_batch_properties(hv):
     scale = np.abs(np.diag(M)).max()
     assert np.all(np.diag(M) > 0)
     assert np.max(np.abs(M - M.T)) <= 1e-4 * scale
+    # storage-mode invariance at full size (P8 on the GPU): BOUNDARY reverses 2000 fp32 leapfrog steps
+    for store in ("checkpoint", "boundary"):
+        alt = hv.Solver.from_workload(wl, shot_batch=2, store=store).hessvec(wl.model, V)
+        assert rel_l2(alt, out) <= TOL, (store, rel_l2(alt, out))
     sub = s.hessvec(wl.model, V[[5, 40]])            # same shot batching -> bitwise identical rows
     assert np.array_equal(sub[0], out[5].astype(np.float32)) and np.array_equal(sub[1], out[40].astype(np.float32))
 
@@ -253,7 +259,7 @@ def test_psido_apply_parity(hv, nz, nx, r):
 # cfg 2 grid and ~0.45 s on the 2088 x 6184 cfg 4 grid); the full-length runs are covered by the properties above.
 
 
-@pytest.mark.parametrize("store", ["full", "checkpoint"])
+@pytest.mark.parametrize("store", ["full", "checkpoint", "boundary"])
 def test_cfg2_full_grid_fused_gradient_hessvec_slice(hv, store):
     wl = W.config(2).subset(shots=[31], nt=300)
     V = wl.probes([0, 1])

@@ -397,7 +397,13 @@ __device__ __forceinline__ void fwd_body(const CUtensorMap* mh, const CUtensorMa
   }
 }
 
-__global__ void __launch_bounds__(NTHREADS, 2)
+#ifndef HV_FWD_MINB
+#define HV_FWD_MINB 2
+#endif
+#ifndef HV_BWD_MINB
+#define HV_BWD_MINB 2
+#endif
+__global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
     fwd_step_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
                     const __grid_constant__ CUtensorMap mq, const FwdParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -590,7 +596,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   }
 }
 
-__global__ void __launch_bounds__(NTHREADS, 2)
+__global__ void __launch_bounds__(NTHREADS, HV_BWD_MINB)
     bwd_step_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
                     const BwdParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];

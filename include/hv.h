@@ -114,6 +114,35 @@ HV_API int hv_gradient_hessvec(hv_ctx* ctx, const float* m, const float* d_obs, 
 HV_API int hv_psido_apply(hv_ctx* ctx, int32_t nz, int32_t nx, int32_t r, const float* a, const float* b,
                    const float* v, float* out, int32_t mode);
 
+/* ---- Probe -> symbol assembly, feeding hv_psido_apply. Discrete conventions: DESIGN.md §3
+ * R-probe (unnormalised DFT, unit-spike probes, periodic interior grid). Complex outputs are interleaved complex64.
+ *
+ * PSF symbol rows: responses [nb][nz][nx] = H_d v_b for probes v_b that are sums of
+ * unit spikes; point k at (pt_iz[k], pt_ix[k]) was probed in batch pt_batch[k]. rows [np][nz][nx] =
+ * conj(DFT(p_k)) with p_k = the (2 radius + 1)^2 window of the response around the point, rolled to the origin
+ * (the paper's s(x_k, xi) = (2 pi)^2 conj(p^_k(xi))). Index arrays may be host or device pointers. */
+HV_API int hv_psf_rows(hv_ctx* ctx, int32_t nz, int32_t nx, int32_t nb, const float* responses, int32_t np,
+                       const int32_t* pt_iz, const int32_t* pt_ix, const int32_t* pt_batch, int32_t radius,
+                       float* rows);
+
+/* PSF spatial weights ("interpolation weights"): bilinear hats on the lattice
+ * lat_z[nlz] x lat_x[nlx] (sorted), constant outside it; w [nlz * nlx][nz][nx], k = i * nlx + j. Partition of
+ * unity; w_k(x_j) = delta_kj. apply_psf == hv_psido_apply(a = w, b = rows). */
+HV_API int hv_psf_weights(hv_ctx* ctx, int32_t nz, int32_t nx, int32_t nlz, const int32_t* lat_z, int32_t nlx,
+                          const int32_t* lat_x, float* w);
+
+/* PDO symbol columns (Eq. equ:symbol): response [nz][nx] = H_d v_p, v_p = sum_k phi_{xi_k};
+ * xi_k given as DFT indices (kz[k], kx[k]); cols [r][nz][nx] = IDFT(M_k . DFT(response)) / phi_{xi_k}, M_k = disc
+ * of mask_radius frequency cells around xi_k with a 2-cell raised-cosine roll-off. */
+HV_API int hv_pdo_columns(hv_ctx* ctx, int32_t nz, int32_t nx, const float* response, int32_t r, const int32_t* kz,
+                          const int32_t* kx, float mask_radius, float* cols);
+
+/* PDO frequency weights (Eq. equ:pdo-w): w [r][nz][nx] (complex64, imaginary 0) =
+ * (|xi| / rho0) t(theta(xi) - theta_k), t(phi) = sin(r phi / 2) cot(phi / 2) / r (r even), xi at the unshifted
+ * DFT frequencies of spacing h, theta = atan2(xi_z, xi_x). apply_pdo == hv_psido_apply(a = Re cols, b = w). */
+HV_API int hv_pdo_weights(hv_ctx* ctx, int32_t nz, int32_t nx, float h, float rho0, int32_t r, const float* thetas,
+                          float* w);
+
 /* Counters of the last call (for benches). */
 typedef struct {
   int64_t kernel_launches;   /* launches of this library's kernels in the last call           */

@@ -78,9 +78,9 @@ def psf_weights(nz: int, nx: int, lat_z: Sequence[int], lat_x: Sequence[int]) ->
 
 
 def freq_index_to_xi(kz: int, kx: int, nz: int, nx: int, h: float) -> Tuple[float, float]:
-    """Angular frequency (xi_z, xi_x) of DFT index (kz, kx) in the unshifted order."""
-    fz = kz - nz if kz > nz // 2 else kz
-    fx = kx - nx if kx > nx // 2 else kx
+    """Angular frequency (xi_z, xi_x) of DFT index (kz, kx), unshifted order, range [-n/2, n/2)."""
+    fz = kz - nz if kz >= (nz + 1) // 2 else kz
+    fx = kx - nx if kx >= (nx + 1) // 2 else kx
     return 2 * math.pi * fz / (nz * h), 2 * math.pi * fx / (nx * h)
 
 

@@ -78,11 +78,16 @@ def lib() -> ctypes.CDLL:
         L.hv_hessvec.argtypes = [vp, fp, i32, fp, fp]
         L.hv_gradient_hessvec.argtypes = [vp, fp, fp, i32, fp, fp, ctypes.POINTER(ctypes.c_double), fp]
         L.hv_psido_apply.argtypes = [vp, i32, i32, i32, fp, fp, fp, fp, i32]
+        L.hv_psf_rows.argtypes = [vp, i32, i32, i32, fp, i32, ip, ip, ip, i32, fp]
+        L.hv_psf_weights.argtypes = [vp, i32, i32, i32, ip, i32, ip, fp]
+        L.hv_pdo_columns.argtypes = [vp, i32, i32, fp, i32, ip, ip, ctypes.c_float, fp]
+        L.hv_pdo_weights.argtypes = [vp, i32, i32, ctypes.c_float, ctypes.c_float, i32, fp, fp]
         L.hv_get_stats.argtypes = [vp, ctypes.POINTER(HvStats)]
         L.hv_last_error.argtypes = [vp]
         L.hv_last_error.restype = ctypes.c_char_p
         for name in ("hv_create", "hv_destroy", "hv_set_stream", "hv_forward", "hv_gradient", "hv_hessvec",
-                     "hv_gradient_hessvec", "hv_psido_apply", "hv_get_stats"):
+                     "hv_gradient_hessvec", "hv_psido_apply", "hv_get_stats", "hv_psf_rows", "hv_psf_weights",
+                     "hv_pdo_columns", "hv_pdo_weights"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -236,6 +241,58 @@ class Solver:
         self._stream(A, B, Vv, o)
         self._check(lib().hv_psido_apply(self._h, nz, nx, r, A.ptr, B.ptr, Vv.ptr, o.ptr, int(mode)))
         return o.obj
+
+    # ---------------------------------------------------------------- probe -> symbol assembly (N1)
+
+    def _cempty(self, ref: _Arr, shape):
+        if _is_torch(ref.obj):
+            import torch
+            return torch.empty(tuple(shape), dtype=torch.complex64, device=ref.obj.device)
+        return np.empty(tuple(shape), dtype=np.complex64)
+
+    def psf_rows(self, responses, points, batch_of, radius: int):
+        """Symbol rows conj(DFT(p_k)) [np][nz][nx] complex64 from PSF responses [nb][nz][nx]."""
+        nb, nz, nx = (int(d) for d in responses.shape)
+        R = _Arr(responses, shape=(nb, nz, nx), name="responses")
+        pts = np.ascontiguousarray(np.asarray(points, dtype=np.int32).reshape(-1, 2))
+        iz, ix = np.ascontiguousarray(pts[:, 0]), np.ascontiguousarray(pts[:, 1])
+        b = np.ascontiguousarray(np.asarray(batch_of, dtype=np.int32))
+        out = _Arr(self._cempty(R, (len(pts), nz, nx)), dtype=np.complex64, name="rows")
+        self._stream(R, out)
+        self._check(lib().hv_psf_rows(self._h, nz, nx, nb, R.ptr, len(pts), iz.ctypes.data, ix.ctypes.data,
+                                      b.ctypes.data, int(radius), out.ptr))
+        return out.obj
+
+    def psf_weights(self, nz: int, nx: int, lat_z, lat_x, like=None):
+        """Bilinear hat weights [len(lat_z) * len(lat_x)][nz][nx]."""
+        lz = np.ascontiguousarray(np.asarray(lat_z, dtype=np.int32))
+        lx = np.ascontiguousarray(np.asarray(lat_x, dtype=np.int32))
+        ref = _Arr(like if like is not None else np.zeros(1, np.float32), name="like")
+        out = _Arr(_empty_like_kind(ref, (len(lz) * len(lx), nz, nx)), name="w")
+        self._stream(out)
+        self._check(lib().hv_psf_weights(self._h, nz, nx, len(lz), lz.ctypes.data, len(lx), lx.ctypes.data, out.ptr))
+        return out.obj
+
+    def pdo_columns(self, response, freq_idx, mask_radius: float):
+        """Symbol columns [r][nz][nx] complex64 by spectral separation."""
+        nz, nx = (int(d) for d in response.shape)
+        R = _Arr(response, shape=(nz, nx), name="response")
+        f = np.ascontiguousarray(np.asarray(freq_idx, dtype=np.int32).reshape(-1, 2))
+        kz, kx = np.ascontiguousarray(f[:, 0]), np.ascontiguousarray(f[:, 1])
+        out = _Arr(self._cempty(R, (len(f), nz, nx)), dtype=np.complex64, name="cols")
+        self._stream(R, out)
+        self._check(lib().hv_pdo_columns(self._h, nz, nx, R.ptr, len(f), kz.ctypes.data, kx.ctypes.data,
+                                         float(mask_radius), out.ptr))
+        return out.obj
+
+    def pdo_weights(self, nz: int, nx: int, h: float, rho0: float, thetas, like=None):
+        """Frequency weights (|xi| / rho0) t(theta - theta_k) [r][nz][nx] complex64."""
+        th = np.ascontiguousarray(np.asarray(thetas, dtype=np.float32))
+        ref = _Arr(like if like is not None else np.zeros(1, np.float32), name="like")
+        out = _Arr(self._cempty(ref, (len(th), nz, nx)), dtype=np.complex64, name="w")
+        self._stream(out)
+        self._check(lib().hv_pdo_weights(self._h, nz, nx, float(h), float(rho0), len(th), th.ctypes.data, out.ptr))
+        return out.obj
 
     def stats(self) -> dict:
         s = HvStats()

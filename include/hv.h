@@ -143,6 +143,23 @@ HV_API int hv_pdo_columns(hv_ctx* ctx, int32_t nz, int32_t nx, const float* resp
 HV_API int hv_pdo_weights(hv_ctx* ctx, int32_t nz, int32_t nx, float h, float rho0, int32_t r, const float* thetas,
                           float* w);
 
+/* ---- High-pass wrapper ("apply a high-pass filter to H_d before the
+ * approximation"): out = Q v for K fields v, out [K][nz][nx], Q = IDFT diag(q) DFT with q(|xi|) = 0 below
+ * cutoff - width/2, 1 above cutoff + width/2, raised cosine between (angular frequencies, grid spacing h). The
+ * wrapped operator Q H_d Q is hv_highpass -> hv_hessvec -> hv_highpass. */
+HV_API int hv_highpass(hv_ctx* ctx, int32_t nz, int32_t nx, float h, float cutoff, float width, int32_t K,
+                       const float* v, float* out);
+
+/* ---- Randomized low-rank generalized eigensolver (Eq. equ:eig):
+ * leading r pairs of H_d v = lambda R v over the shard's shots, V^T R V = I, with R = (delta I - gamma Delta)^2 the
+ * biharmonic prior precision applied as the periodic spectral multiplier (delta + gamma |xi|^2)^2.
+ * Double-pass randomized algorithm with power_iters power iterations; each pass is ONE batched hv_hessvec on
+ * K = r + oversampling probes. Omega [K][nz][nx] are the caller's random probes (e.g. N(0,1) draws).
+ * evals [r] float64 descending (host or device), evecs [r][nz][nx] float32 (may be NULL). Multi-GPU note: the
+ * eigensolve needs the FULL H_d, so call it on a context whose shard covers every shot. */
+HV_API int hv_lowrank_geneig(hv_ctx* ctx, const float* m, int32_t r, int32_t K, const float* Omega,
+                             int32_t power_iters, double delta, double gamma, double* evals, float* evecs);
+
 /* Counters of the last call (for benches). */
 typedef struct {
   int64_t kernel_launches;   /* launches of this library's kernels in the last call           */

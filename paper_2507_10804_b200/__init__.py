@@ -82,12 +82,14 @@ def lib() -> ctypes.CDLL:
         L.hv_psf_weights.argtypes = [vp, i32, i32, i32, ip, i32, ip, fp]
         L.hv_pdo_columns.argtypes = [vp, i32, i32, fp, i32, ip, ip, ctypes.c_float, fp]
         L.hv_pdo_weights.argtypes = [vp, i32, i32, ctypes.c_float, ctypes.c_float, i32, fp, fp]
+        L.hv_highpass.argtypes = [vp, i32, i32, ctypes.c_float, ctypes.c_float, ctypes.c_float, i32, fp, fp]
+        L.hv_lowrank_geneig.argtypes = [vp, fp, i32, i32, fp, i32, ctypes.c_double, ctypes.c_double, fp, fp]
         L.hv_get_stats.argtypes = [vp, ctypes.POINTER(HvStats)]
         L.hv_last_error.argtypes = [vp]
         L.hv_last_error.restype = ctypes.c_char_p
         for name in ("hv_create", "hv_destroy", "hv_set_stream", "hv_forward", "hv_gradient", "hv_hessvec",
                      "hv_gradient_hessvec", "hv_psido_apply", "hv_get_stats", "hv_psf_rows", "hv_psf_weights",
-                     "hv_pdo_columns", "hv_pdo_weights"):
+                     "hv_pdo_columns", "hv_pdo_weights", "hv_highpass", "hv_lowrank_geneig"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -293,6 +295,37 @@ class Solver:
         self._stream(out)
         self._check(lib().hv_pdo_weights(self._h, nz, nx, float(h), float(rho0), len(th), th.ctypes.data, out.ptr))
         return out.obj
+
+    # ---------------------------------------------------------------- high-pass wrapper (N4)
+
+    def highpass(self, V, h: float, cutoff: float, width: float, out=None):
+        """Q v for V [K][nz][nx] (or [nz][nx]): raised-cosine high-pass multiplier."""
+        squeeze = V.ndim == 2
+        K, nz, nx = (1, *V.shape) if squeeze else tuple(int(d) for d in V.shape)
+        v = _Arr(V.reshape(K, nz, nx) if squeeze else V, shape=(K, nz, nx), name="V")
+        o = _Arr(out if out is not None else _empty_like_kind(v, (K, nz, nx)), shape=(K, nz, nx), name="out")
+        self._stream(v, o)
+        self._check(lib().hv_highpass(self._h, nz, nx, float(h), float(cutoff), float(width), K, v.ptr, o.ptr))
+        return o.obj.reshape(nz, nx) if squeeze else o.obj
+
+    def hessvec_highpass(self, m, V, h: float, cutoff: float, width: float):
+        """Q H_d Q [v_1..v_K]: the high-pass-filtered Hessian the PSF / PDO approximations target."""
+        return self.highpass(self.hessvec(m, self.highpass(V, h, cutoff, width)), h, cutoff, width)
+
+    # ---------------------------------------------------------------- randomized generalized eigensolver (N2)
+
+    def lowrank_geneig(self, m, Omega, r: int, power_iters: int = 1, delta: float = 1.0, gamma: float = 0.0):
+        """Leading r pairs of H_d v = lambda R v, R = (delta I - gamma Delta)^2.
+        Omega: [K][nz][nx] random probes, K >= r. Returns (evals float64 [r] descending, evecs [r][nz][nx])."""
+        a = _Arr(m, shape=(self.nz, self.nx), name="m")
+        K = int(Omega.shape[0])
+        om = _Arr(Omega, shape=(K, self.nz, self.nx), name="Omega")
+        ev = np.zeros(r, dtype=np.float64)
+        V = _Arr(_empty_like_kind(om, (r, self.nz, self.nx)), name="evecs")
+        self._stream(a, om, V)
+        self._check(lib().hv_lowrank_geneig(self._h, a.ptr, int(r), K, om.ptr, int(power_iters), float(delta),
+                                            float(gamma), ev.ctypes.data, V.ptr))
+        return ev, V.obj
 
     def stats(self) -> dict:
         s = HvStats()

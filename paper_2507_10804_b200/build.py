@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhv.so")
-SOURCES = ["hv_api.cu", "hv_runtime.cu", "psido.cu", "probing.cu"]
+SOURCES = ["hv_api.cu", "hv_runtime.cu", "psido.cu", "probing.cu", "lowrank.cu"]
 HEADERS = ["hv_kernels.cuh", "hv_geo.h", "hv_internal.h", os.path.join("..", "..", "include", "hv.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -43,7 +43,7 @@ def build(force: bool = False, ptxas_verbose: bool = False, out: str = LIB, defi
            "-Xcompiler", "-fvisibility=hidden",
            *[f"-D{d}" for d in defines],
            "-o", out + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES],
-           "-lcufft", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+           "-lcufft", "-lcublas", "-lcusolver", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     if ptxas_verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)

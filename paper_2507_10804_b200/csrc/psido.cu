@@ -62,6 +62,36 @@ __global__ void psido_real_out(long long n, const cufftComplex* __restrict__ Z, 
     out[q] = accumulate ? out[q] + scale * cuCrealf(Z[q]) : scale * cuCrealf(Z[q]);
 }
 
+// High-pass multiplier q(|xi|) (raised cosine between cutoff -+ width/2), applied in place to K spectra; scale 1/N
+__global__ void highpass_mul(int nz, int nx, int K, float h, float cutoff, float width, cufftComplex* __restrict__ T) {
+  const long long n = (long long)nz * nx;
+  const float lo = cutoff - 0.5f * width, hi = cutoff + 0.5f * width;
+  const float inv_n = 1.0f / static_cast<float>(n);
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n * K; q += (long long)gridDim.x * blockDim.x) {
+    const int rem = static_cast<int>(q % n);
+    const int z = rem / nx, x = rem % nx;
+    const int fz = z >= (nz + 1) / 2 ? z - nz : z, fx = x >= (nx + 1) / 2 ? x - nx : x;
+    const float xz = 6.283185307179586f * fz / (nz * h), xx = 6.283185307179586f * fx / (nx * h);
+    const float rho = sqrtf(xz * xz + xx * xx);
+    float m;
+    if (rho >= hi) m = 1.0f;
+    else if (rho <= lo) m = 0.0f;
+    else m = 0.5f * (1.0f - cospif((rho - lo) / width));
+    m *= inv_n;
+    T[q] = make_cuFloatComplex(m * T[q].x, m * T[q].y);
+  }
+}
+
+__global__ void real_part_out(long long n, const cufftComplex* __restrict__ T, float* __restrict__ out) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x)
+    out[q] = cuCrealf(T[q]);
+}
+
+__global__ void reals_to_complex(long long n, const float* __restrict__ v, cufftComplex* __restrict__ X) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x)
+    X[q] = make_cuFloatComplex(v[q], 0.0f);
+}
+
 int grid_for(long long n) { return static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16)); }
 
 int get_plan(hv_ctx* c, int nz, int nx, int batch, cufftHandle* out) {
@@ -128,5 +158,36 @@ extern "C" int hv_psido_apply(hv_ctx* c, int32_t nz, int32_t nx, int32_t r, cons
   CU_TRY(cudaStreamSynchronize(c->stream));
   c->stats = hv_stats{};
   c->stats.kernel_launches = launches;
+  return HV_OK;
+}
+
+// High-pass filter Q = IDFT diag(q) DFT on K fields. v, out [K][nz][nx].
+extern "C" int hv_highpass(hv_ctx* c, int32_t nz, int32_t nx, float h, float cutoff, float width, int32_t K,
+                           const float* v_in, float* out_user) {
+  if (!c) return HV_ESTATE;
+  c->err.clear();
+  if (nz < 1 || nx < 1 || K < 1) return fail(c, HV_EGRID, "bad sizes");
+  if (!(h > 0.0f) || !(width > 0.0f) || !(cutoff >= 0.0f)) return fail(c, HV_EINVAL, "bad filter parameters");
+  CU_TRY(cudaSetDevice(c->dev));
+  const long long n = (long long)nz * nx;
+  const float* v;
+  int st;
+  if ((st = stage_in(c, "hp_v", v_in, sizeof(float) * n * K, (const void**)&v))) return st;
+  OutStage o;
+  if ((st = stage_out(c, "hp_out", out_user, sizeof(float) * n * K, &o))) return st;
+  cufftComplex* T;
+  if ((st = ws_get(c, "hp_T", sizeof(cufftComplex) * n * K, (void**)&T))) return st;
+  cufftHandle p;
+  if ((st = get_plan(c, nz, nx, K, &p))) return st;
+  reals_to_complex<<<grid_for(n * K), 256, 0, c->stream>>>(n * K, v, T);
+  if (cufftExecC2C(p, T, T, CUFFT_FORWARD) != CUFFT_SUCCESS) return fail(c, HV_ECUDA, "cufftExecC2C");
+  highpass_mul<<<grid_for(n * K), 256, 0, c->stream>>>(nz, nx, K, h, cutoff, width, T);
+  if (cufftExecC2C(p, T, T, CUFFT_INVERSE) != CUFFT_SUCCESS) return fail(c, HV_ECUDA, "cufftExecC2C");
+  real_part_out<<<grid_for(n * K), 256, 0, c->stream>>>(n * K, T, reinterpret_cast<float*>(o.dev));
+  CU_TRY(cudaGetLastError());
+  if ((st = finish_out(c, o))) return st;
+  CU_TRY(cudaStreamSynchronize(c->stream));
+  c->stats = hv_stats{};
+  c->stats.kernel_launches = 3;
   return HV_OK;
 }

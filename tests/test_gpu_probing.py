@@ -95,3 +95,43 @@ def test_pdo_pipeline_on_hessvec_cfg1(hv):
     out = s.psido_apply(a, w, v, 2)
     ref = opsido.apply_symmetric(cref.real, opr.pdo_weights(wl.nz, wl.nx, wl.h, rho0, th), v.astype(np.float64))
     assert rel_l2(out, ref) <= TOL
+
+
+def test_highpass_parity_and_wrapped_hessian(hv):
+    from oracle import highpass as ohp
+    from oracle import wave
+    rng = np.random.default_rng(3)
+    V = rng.standard_normal((3, 40, 56)).astype(np.float32)
+    s = hv.Solver.from_workload(W.config(0))
+    out = s.highpass(V, 10.0, 0.05, 0.03)
+    assert rel_l2(out, ohp.apply(V.astype(np.float64), 10.0, 0.05, 0.03)) <= TOL
+    # wrapped operator Q H Q on cfg 0 against the oracle's Q H Q (and it stays symmetric)
+    wl = W.config(0)
+    P = np.stack([wl.probe_fn(0), W.gaussian_probe((64, 64), 11, 2.0)])
+    got = s.hessvec_highpass(wl.model, P, wl.h, 0.02, 0.01)
+    ref = ohp.wrap(lambda X: wave.Problem(wl).hessvec(list(X)), wl.h, 0.02, 0.01)(P.astype(np.float64))
+    assert rel_l2(got, ref) <= TOL
+    a, b = float(np.sum(P[1] * got[0])), float(np.sum(P[0] * got[1]))
+    assert abs(a - b) <= 1e-4 * max(abs(a), abs(b))
+
+
+def test_lowrank_geneig_parity_cfg0(hv):
+    """N2: randomized generalized eigensolver on the cfg 0 H_d with the same Omega on both sides."""
+    from oracle import lowrank as olr
+    from oracle import wave
+    wl = W.config(0)
+    K, r, q = 12, 6, 1
+    Om = np.stack([W.gaussian_probe((64, 64), 100 + k, 1.0) for k in range(K)])
+    delta, gamma = 1.0, 4.0 * wl.h ** 2
+    s = hv.Solver.from_workload(wl)
+    ev, V = s.lowrank_geneig(wl.model, Om, r, power_iters=q, delta=delta, gamma=gamma)
+    pb = wave.Problem(wl)
+    lam, Vr = olr.randomized_gen_eig(lambda X: pb.hessvec(list(X)), Om.astype(np.float64), r, q, wl.h, delta, gamma)
+    assert np.all(np.diff(ev) <= 0)
+    assert np.max(np.abs(ev - lam) / lam[0]) <= 1e-4, (ev, lam)
+    RV = olr.prior_apply(Vr, wl.h, delta, gamma)
+    for i in range(r):
+        gap = min(abs(lam[i] - lam[j]) for j in range(r) if j != i) / lam[0]
+        if gap > 1e-2:
+            c = abs(float(np.sum(V[i].astype(np.float64) * RV[i])))
+            assert abs(c - 1.0) <= 1e-3, (i, c)

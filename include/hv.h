@@ -110,7 +110,9 @@ HV_API int hv_gradient_hessvec(hv_ctx* ctx, const float* m, const float* d_obs, 
  *   mode 2: (mode 0 + mode 1) / 2                             (symmetrised)
  * a [r][nz][nx] float32 (real spatial factors), b [r][nz][nx] interleaved complex64 (frequency factors at the
  * unshifted DFT frequencies), v, out [nz][nx]. DFT unnormalised, IDFT scaled 1/(nz nx), so b == 1 is the
- * identity. apply_psf == (a = PSF weights w_k, b = symbol rows); apply_pdo == (a = symbol columns, b = weights). */
+ * identity. apply_psf == (a = PSF weights w_k, b = symbol rows); apply_pdo == (a = symbol columns, b = weights).
+ * mode + 4: the spatial factors a are interleaved complex64 [r][nz][nx] (PSF+ factors); out = Re sum_k a_k . IDFT(..),
+ * adjoint Re sum_k IDFT(conj(b_k) . DFT(conj(a_k) . v)). */
 HV_API int hv_psido_apply(hv_ctx* ctx, int32_t nz, int32_t nx, int32_t r, const float* a, const float* b,
                    const float* v, float* out, int32_t mode);
 
@@ -159,6 +161,16 @@ HV_API int hv_highpass(hv_ctx* ctx, int32_t nz, int32_t nx, float h, float cutof
  * eigensolve needs the FULL H_d, so call it on a context whose shard covers every shot. */
 HV_API int hv_lowrank_geneig(hv_ctx* ctx, const float* m, int32_t r, int32_t K, const float* Omega,
                              int32_t power_iters, double delta, double gamma, double* evals, float* evecs);
+
+/* ---- PSF+ (Eq. equ:psfplus): from symbol rows [nr][nz][nx] (complex64,
+ * hv_psf_rows), their PSF weights w [nr][nz][nx] (hv_psf_weights) and symbol columns [nc][nz][nx] (complex64,
+ * hv_pdo_columns) at DFT indices (col_kz, col_kx): B = leading `rank` right singular vectors of the rows,
+ * A_0 = W U_r Sigma_r, A = (S_c B_c^H + alpha A_0)(B_c B_c^H + alpha I)^-1 with alpha = ||B_c||^2 / ||B||^2.
+ * Outputs A [rank][nz][nx] (column k = a_k, complex64), B [rank][nz][nx] (complex64), *alpha (may be NULL).
+ * Apply with hv_psido_apply(a = A, b = B, mode + 4). */
+HV_API int hv_psf_plus(hv_ctx* ctx, int32_t nz, int32_t nx, int32_t nr, const float* rows, const float* w, int32_t nc,
+                       const float* cols, const int32_t* col_kz, const int32_t* col_kx, int32_t rank, float* A,
+                       float* B, double* alpha);
 
 /* Counters of the last call (for benches). */
 typedef struct {

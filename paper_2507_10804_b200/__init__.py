@@ -84,12 +84,14 @@ def lib() -> ctypes.CDLL:
         L.hv_pdo_weights.argtypes = [vp, i32, i32, ctypes.c_float, ctypes.c_float, i32, fp, fp]
         L.hv_highpass.argtypes = [vp, i32, i32, ctypes.c_float, ctypes.c_float, ctypes.c_float, i32, fp, fp]
         L.hv_lowrank_geneig.argtypes = [vp, fp, i32, i32, fp, i32, ctypes.c_double, ctypes.c_double, fp, fp]
+        L.hv_psf_plus.argtypes = [vp, i32, i32, i32, fp, fp, i32, fp, ip, ip, i32, fp, fp,
+                                  ctypes.POINTER(ctypes.c_double)]
         L.hv_get_stats.argtypes = [vp, ctypes.POINTER(HvStats)]
         L.hv_last_error.argtypes = [vp]
         L.hv_last_error.restype = ctypes.c_char_p
         for name in ("hv_create", "hv_destroy", "hv_set_stream", "hv_forward", "hv_gradient", "hv_hessvec",
                      "hv_gradient_hessvec", "hv_psido_apply", "hv_get_stats", "hv_psf_rows", "hv_psf_weights",
-                     "hv_pdo_columns", "hv_pdo_weights", "hv_highpass", "hv_lowrank_geneig"):
+                     "hv_pdo_columns", "hv_pdo_weights", "hv_highpass", "hv_lowrank_geneig", "hv_psf_plus"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -234,9 +236,12 @@ class Solver:
         return phi.value, g.obj, o.obj
 
     def psido_apply(self, a, b, v, mode: int = 0, out=None):
-        """Low-rank-symbol PsiDO apply: a [r][nz][nx] real, b [r][nz][nx] complex64, v [nz][nx]."""
+        """Low-rank-symbol PsiDO apply: a [r][nz][nx] real (or complex64: PSF+ factors),
+        b [r][nz][nx] complex64, v [nz][nx]; mode 0 apply, 1 adjoint, 2 symmetrised."""
         r, nz, nx = (int(s) for s in a.shape)
-        A = _Arr(a, shape=(r, nz, nx), name="a")
+        cplx = np.iscomplexobj(a) if not _is_torch(a) else a.is_complex()
+        A = _Arr(a, dtype=np.complex64 if cplx else np.float32, shape=(r, nz, nx), name="a")
+        mode = int(mode) | (4 if cplx else 0)
         B = _Arr(b, dtype=np.complex64, shape=(r, nz, nx), name="b")
         Vv = _Arr(v, shape=(nz, nx), name="v")
         o = _Arr(out if out is not None else _empty_like_kind(Vv, (nz, nx)), shape=(nz, nx), name="out")
@@ -326,6 +331,25 @@ class Solver:
         self._check(lib().hv_lowrank_geneig(self._h, a.ptr, int(r), K, om.ptr, int(power_iters), float(delta),
                                             float(gamma), ev.ctypes.data, V.ptr))
         return ev, V.obj
+
+    # ---------------------------------------------------------------- PSF+ (N3)
+
+    def psf_plus(self, rows, w, cols, col_idx, rank: int):
+        """PSF+ factors (A [rank][nz][nx], B [rank][nz][nx]) complex64 and alpha (PAPER.md:330-357)."""
+        nr, nz, nx = (int(d) for d in rows.shape)
+        R = _Arr(rows, dtype=np.complex64, shape=(nr, nz, nx), name="rows")
+        Wt = _Arr(w, shape=(nr, nz, nx), name="w")
+        nc = int(cols.shape[0])
+        C = _Arr(cols, dtype=np.complex64, shape=(nc, nz, nx), name="cols")
+        f = np.ascontiguousarray(np.asarray(col_idx, dtype=np.int32).reshape(-1, 2))
+        kz, kx = np.ascontiguousarray(f[:, 0]), np.ascontiguousarray(f[:, 1])
+        A = _Arr(self._cempty(R, (rank, nz, nx)), dtype=np.complex64, name="A")
+        B = _Arr(self._cempty(R, (rank, nz, nx)), dtype=np.complex64, name="B")
+        alpha = ctypes.c_double(0.0)
+        self._stream(R, Wt, C, A, B)
+        self._check(lib().hv_psf_plus(self._h, nz, nx, nr, R.ptr, Wt.ptr, nc, C.ptr, kz.ctypes.data, kx.ctypes.data,
+                                      int(rank), A.ptr, B.ptr, ctypes.byref(alpha)))
+        return A.obj, B.obj, alpha.value
 
     def stats(self) -> dict:
         s = HvStats()

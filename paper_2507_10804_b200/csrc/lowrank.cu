@@ -1,5 +1,5 @@
 // lowrank.cu — randomized low-rank generalized eigensolver H_d v = lambda R v (PAPER.md:168-195,
-// Eq. equ:eig). Double pass with power iterations (the algorithm oracle/lowrank.py restates):
+// Eq. equ:eig). Double pass with power iterations (N2):
 //   Y = R^-1 H_d Omega; [Q = R-orth(Y); Y = R^-1 H_d Q] x power_iters; Q = R-orth(Y); T = Q^T H_d Q = U L U^T;
 //   V = Q U (leading r).
 // H_d products: this library's batched hv_hessvec (one call per pass, K = r + oversampling probes).

@@ -27,22 +27,37 @@ __global__ void psido_symbol_mul(long long n, int r, const cufftComplex* __restr
     T[q] = cuCmulf(b[q], X[q % n]);
 }
 
-// out[p] (+)= scale * sum_k a_k[p] Re T[k][p]
-__global__ void psido_combine(long long n, int r, const float* __restrict__ a, const cufftComplex* __restrict__ T,
-                              float scale, int accumulate, float* __restrict__ out) {
+// out[p] (+)= scale * sum_k Re(a_k[p] T[k][p])   (a real, or complex when ca)
+__global__ void psido_combine(long long n, int r, const float* __restrict__ a, int ca,
+                              const cufftComplex* __restrict__ T, float scale, int accumulate, float* __restrict__ out) {
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
     float s = 0.0f;
-    for (int k = 0; k < r; ++k) s = fmaf(a[k * n + q], cuCrealf(T[k * n + q]), s);
+    for (int k = 0; k < r; ++k) {
+      const cufftComplex t = T[k * n + q];
+      if (ca) {
+        const float2 ak = reinterpret_cast<const float2*>(a)[k * n + q];
+        s = fmaf(ak.x, t.x, fmaf(-ak.y, t.y, s));
+      } else {
+        s = fmaf(a[k * n + q], cuCrealf(t), s);
+      }
+    }
     out[q] = accumulate ? out[q] + scale * s : scale * s;
   }
 }
 
-// Y[k][p] = a_k[p] v[p]
-__global__ void psido_weight(long long n, int r, const float* __restrict__ a, const float* __restrict__ v,
+// Y[k][p] = conj(a_k[p]) v[p]   (a real, or complex when ca)
+__global__ void psido_weight(long long n, int r, const float* __restrict__ a, int ca, const float* __restrict__ v,
                              cufftComplex* __restrict__ Y) {
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n * r;
-       q += (long long)gridDim.x * blockDim.x)
-    Y[q] = make_cuFloatComplex(a[q] * v[q % n], 0.0f);
+       q += (long long)gridDim.x * blockDim.x) {
+    const float vv = v[q % n];
+    if (ca) {
+      const float2 ak = reinterpret_cast<const float2*>(a)[q];
+      Y[q] = make_cuFloatComplex(ak.x * vv, -ak.y * vv);
+    } else {
+      Y[q] = make_cuFloatComplex(a[q] * vv, 0.0f);
+    }
+  }
 }
 
 // Z[p] = sum_k conj(b_k[p]) Y[k][p]
@@ -117,12 +132,14 @@ extern "C" int hv_psido_apply(hv_ctx* c, int32_t nz, int32_t nx, int32_t r, cons
   c->err.clear();
   if (nz < 1 || nx < 1) return fail(c, HV_EGRID, "bad grid");
   if (r < 1) return fail(c, HV_EINVAL, "r must be >= 1");
-  if (mode < 0 || mode > 2) return fail(c, HV_EINVAL, "mode must be 0, 1 or 2");
+  const int ca = (mode & 4) ? 1 : 0;  // complex spatial factors (PSF+)
+  mode &= 3;
+  if (mode > 2) return fail(c, HV_EINVAL, "mode must be 0, 1 or 2 (+4 for complex a)");
   CU_TRY(cudaSetDevice(c->dev));
   const long long n = (long long)nz * nx;
   const float *a, *b, *v;
   int st;
-  if ((st = stage_in(c, "psido_a", a_in, sizeof(float) * n * r, (const void**)&a))) return st;
+  if ((st = stage_in(c, "psido_a", a_in, sizeof(float) * n * r * (ca ? 2 : 1), (const void**)&a))) return st;
   if ((st = stage_in(c, "psido_b", b_in, sizeof(cufftComplex) * n * r, (const void**)&b))) return st;
   if ((st = stage_in(c, "psido_v", v_in, sizeof(float) * n, (const void**)&v))) return st;
   OutStage o;
@@ -142,11 +159,11 @@ extern "C" int hv_psido_apply(hv_ctx* c, int32_t nz, int32_t nx, int32_t r, cons
     if (cufftExecC2C(p1, X, X, CUFFT_FORWARD) != CUFFT_SUCCESS) return fail(c, HV_ECUDA, "cufftExecC2C");
     psido_symbol_mul<<<grid_for(n * r), 256, 0, c->stream>>>(n, r, bc, X, T);
     if (cufftExecC2C(pr, T, T, CUFFT_INVERSE) != CUFFT_SUCCESS) return fail(c, HV_ECUDA, "cufftExecC2C");
-    psido_combine<<<grid_for(n), 256, 0, c->stream>>>(n, r, a, T, half * inv_n, 0, out);
+    psido_combine<<<grid_for(n), 256, 0, c->stream>>>(n, r, a, ca, T, half * inv_n, 0, out);
     launches += 3;
   }
   if (mode == 1 || mode == 2) {
-    psido_weight<<<grid_for(n * r), 256, 0, c->stream>>>(n, r, a, v, T);
+    psido_weight<<<grid_for(n * r), 256, 0, c->stream>>>(n, r, a, ca, v, T);
     if (cufftExecC2C(pr, T, T, CUFFT_FORWARD) != CUFFT_SUCCESS) return fail(c, HV_ECUDA, "cufftExecC2C");
     psido_conj_reduce<<<grid_for(n), 256, 0, c->stream>>>(n, r, bc, T, X);
     if (cufftExecC2C(p1, X, X, CUFFT_INVERSE) != CUFFT_SUCCESS) return fail(c, HV_ECUDA, "cufftExecC2C");

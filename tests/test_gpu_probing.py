@@ -56,45 +56,105 @@ def test_pdo_columns_weights_parity(solver):
     assert rel_l2(w, wref) <= TOL and np.max(np.abs(w.imag)) == 0.0
 
 
-def test_psf_pipeline_on_hessvec_cfg1(hv):
-    """End to end on the bench workload's probes (cfg 1, 2 shots to keep the oracle cheap is not needed: the
-    pipeline input is the GPU's own H·v, and each stage is checked against the oracle applied to the same
-    input): H·v on 4 spikes -> rows -> hat weights -> apply_psf on a smooth probe."""
-    wl = W.config(1).subset(shots=[3, 12])
-    ks = [2 * 8 + 2, 2 * 8 + 5, 5 * 8 + 2, 5 * 8 + 5]
-    V = wl.probes(ks)
+def _cfg0_spikes():
+    """cfg 0 grid and acquisition with 4 PSF spikes on a 2 x 2 lattice (each side computes its own H·v)."""
+    wl = W.config(0)
+    pts = [(20, 20), (20, 44), (44, 20), (44, 44)]
+    V = np.stack([W.spike_probe((64, 64), *p) for p in pts])
+    return wl, pts, V
+
+
+@pytest.fixture(scope="module")
+def cfg0_psf_oracle():
+    from oracle import wave
+    wl, pts, V = _cfg0_spikes()
+    HV = wave.Problem(wl).hessvec(list(V.astype(np.float64)))
+    rows = opr.psf_symbol_rows(opr.extract_psfs(HV, pts, [0, 1, 2, 3], 12))
+    w = opr.psf_weights(64, 64, [20, 44], [20, 44])
+    return wl, pts, V, HV, rows, w
+
+
+@pytest.fixture(scope="module")
+def cfg0_pdo_oracle():
+    from oracle import wave
+    wl = W.config(0)
+    rho0 = 2 * math.pi * 0.0125
+    idx, th = opr.pdo_plan(64, 64, wl.h, rho0, r=8)
+    vp = opr.sinusoid_probe(64, 64, idx).real.astype(np.float32)
+    R = wave.Problem(wl).hessvec([vp.astype(np.float64)])[0]
+    cols = opr.extract_symbol_columns(R, idx, 2.5)
+    wts = opr.pdo_weights(64, 64, wl.h, rho0, th)
+    return wl, rho0, idx, th, vp, cols, wts
+
+
+def test_psf_pipeline_end_to_end(hv, cfg0_psf_oracle):
+    """H·v on 4 spikes -> rows -> hat weights -> apply_psf, each side from its own H·v."""
+    wl, pts, V, HV_ref, rows_ref, w_ref = cfg0_psf_oracle
     s = hv.Solver.from_workload(wl)
     HV = s.hessvec(wl.model, V)
-    pts = [tuple(int(c) for c in np.argwhere(v)[0]) for v in V]
-    rows = s.psf_rows(HV, pts, [0, 1, 2, 3], radius=20)
-    rows_ref = opr.psf_symbol_rows(opr.extract_psfs(HV.astype(np.float64), pts, [0, 1, 2, 3], 20))
+    rows = s.psf_rows(HV, pts, [0, 1, 2, 3], radius=12)
     assert rel_l2(rows, rows_ref) <= TOL
-    lz = sorted({p[0] for p in pts})
-    lx = sorted({p[1] for p in pts})
-    w = s.psf_weights(wl.nz, wl.nx, lz, lx)
-    v = W.gaussian_probe((wl.nz, wl.nx), 5, 4.0)
+    w = s.psf_weights(64, 64, [20, 44], [20, 44])
+    v = W.gaussian_probe((64, 64), 5, 3.0)
     out = s.psido_apply(w, rows, v, 0)
-    ref = opsido.apply(opr.psf_weights(wl.nz, wl.nx, lz, lx), rows_ref, v.astype(np.float64))
+    ref = opsido.apply(w_ref, rows_ref, v.astype(np.float64))
     assert rel_l2(out, ref) <= TOL
 
 
-def test_pdo_pipeline_on_hessvec_cfg1(hv):
-    """H·v on the cosine-sum probe of an 8-angle plan -> columns -> weights -> apply_pdo."""
-    wl = W.config(1).subset(shots=[7])
-    rho0 = 2 * math.pi * 0.012
-    idx, th = opr.pdo_plan(wl.nz, wl.nx, wl.h, rho0, r=8)
-    vp = opr.sinusoid_probe(wl.nz, wl.nx, idx).real.astype(np.float32)
+def test_pdo_pipeline_end_to_end(hv, cfg0_pdo_oracle):
+    """H·v on the 8-angle cosine-sum probe -> columns -> weights -> apply_pdo (symmetrised)."""
+    wl, rho0, idx, th, vp, cref, wref = cfg0_pdo_oracle
     s = hv.Solver.from_workload(wl)
     R = s.hessvec(wl.model, vp[None])[0]
-    cols = s.pdo_columns(R, idx, mask_radius=4.0)
-    cref = opr.extract_symbol_columns(R.astype(np.float64), idx, 4.0)
+    cols = s.pdo_columns(R, idx, mask_radius=2.5)
     assert rel_l2(cols, cref) <= TOL
-    w = s.pdo_weights(wl.nz, wl.nx, wl.h, rho0, th)
-    a = np.ascontiguousarray(cols.real)
-    v = W.gaussian_probe((wl.nz, wl.nx), 9, 3.0)
-    out = s.psido_apply(a, w, v, 2)
-    ref = opsido.apply_symmetric(cref.real, opr.pdo_weights(wl.nz, wl.nx, wl.h, rho0, th), v.astype(np.float64))
+    w = s.pdo_weights(64, 64, wl.h, rho0, th)
+    v = W.gaussian_probe((64, 64), 9, 3.0)
+    out = s.psido_apply(np.ascontiguousarray(cols.real), w, v, 2)
+    ref = opsido.apply_symmetric(cref.real, wref, v.astype(np.float64))
     assert rel_l2(out, ref) <= TOL
+
+
+def test_psf_plus_synthetic_parity(solver):
+    from oracle import psfplus as opp
+    rng = np.random.default_rng(4)
+    nz, nx, nr, nc, rank = 24, 32, 6, 4, 3
+    N = nz * nx
+    Bt = np.linalg.qr(rng.standard_normal((N, 4)) + 1j * rng.standard_normal((N, 4)))[0].T
+    rows = ((rng.standard_normal((nr, 4)) + 1j * rng.standard_normal((nr, 4))) @ Bt).reshape(nr, nz, nx)
+    rows = (rows + 1e-3 * (rng.standard_normal(rows.shape) + 1j * rng.standard_normal(rows.shape))).astype(np.complex64)
+    w = rng.random((nr, nz, nx)).astype(np.float32)
+    cols = (rng.standard_normal((nc, nz, nx)) + 1j * rng.standard_normal((nc, nz, nx))).astype(np.complex64)
+    idx = [(1, 2), (3, 7), (5, 1), (20, 30)]
+    A, B, alpha = solver.psf_plus(rows, w, cols, idx, rank)
+    Ar, Br, aref = opp.psf_plus(rows.astype(np.complex128), w.astype(np.float64), cols.astype(np.complex128), idx, rank)
+    assert abs(alpha - aref) <= 1e-5 * aref
+    v = rng.standard_normal((nz, nx)).astype(np.float32)
+    out = solver.psido_apply(A, B, v, 0)
+    ref = opp.apply(Ar, Br, v.astype(np.float64))
+    assert rel_l2(out, ref) <= TOL
+    # the factorisation is unique up to per-column phases: compare the symbol A B at sampled (x, xi)
+    S = np.einsum("kx,ky->xy", A.reshape(rank, N)[:, ::97], B.reshape(rank, N)[:, ::89])
+    Sr = np.einsum("xk,ky->xy", Ar[::97], Br[:, ::89])
+    assert rel_l2(S, Sr) <= TOL
+
+
+def test_psf_plus_pipeline_end_to_end(hv, cfg0_psf_oracle, cfg0_pdo_oracle):
+    """PSF rows + PDO columns of the cfg 0 H_d (each side from its own H·v) -> PSF+ rank 3 -> apply."""
+    from oracle import psfplus as opp
+    wl, pts, V, HV_ref, rows_ref, w_ref = cfg0_psf_oracle
+    _, rho0, idx, th, vp, cref, wref = cfg0_pdo_oracle
+    s = hv.Solver.from_workload(wl)
+    HV = s.hessvec(wl.model, V)
+    rows = s.psf_rows(HV, pts, [0, 1, 2, 3], radius=12)
+    w = s.psf_weights(64, 64, [20, 44], [20, 44])
+    R = s.hessvec(wl.model, vp[None])[0]
+    cols = s.pdo_columns(R, idx, mask_radius=2.5)
+    A, B, alpha = s.psf_plus(rows, w, cols, idx, 3)
+    Ar, Br, aref = opp.psf_plus(rows_ref, w_ref, cref, idx, 3)
+    assert abs(alpha - aref) <= 1e-4 * aref
+    v = W.gaussian_probe((64, 64), 13, 3.0)
+    assert rel_l2(s.psido_apply(A, B, v, 0), opp.apply(Ar, Br, v.astype(np.float64))) <= TOL
 
 
 def test_highpass_parity_and_wrapped_hessian(hv):

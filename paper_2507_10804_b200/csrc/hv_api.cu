@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -233,19 +234,24 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   const dim3 tiles(g.ntx, g.ntz);
   double ms_f = 0, ms_b = 0;
   std::vector<cudaEvent_t> evs;
+  int64_t graph_launches = 0;
   auto new_event = [&](cudaEvent_t* e) -> int {
     CU_TRY(cudaEventCreate(e));
     evs.push_back(*e);
     return HV_OK;
   };
 
-  for (int b0 = 0; b0 < nloc; b0 += S) {
-    const int Sb = std::min(S, nloc - b0);
-    cudaEvent_t e_f0, e_f1, e_b0, e_b1;
-    if ((st = new_event(&e_f0)) || (st = new_event(&e_f1)) || (st = new_event(&e_b0)) || (st = new_event(&e_b1)))
-      return st;
-    CU_TRY(cudaMemsetAsync(pool, 0, sizeof(float) * g.plane * planes_per_shot * Sb, c->stream));
-    CU_TRY(cudaEventRecord(e_f0, c->stream));
+  // One shot batch = one enqueue of the whole time loop (forward sweep, checkpoint saves / replays, backward
+  // sweep). It is captured once into a CUDA graph per (call signature, buffers) and replayed afterwards.
+  int64_t batch_launches = 0;
+  // phase 0: forward sweep (+ gather); phase 1: backward sweep. Events may be null (recorded by the caller).
+  auto enqueue_batch = [&](int phase, int b0, int Sb, cudaEvent_t e_f0, cudaEvent_t e_f1, cudaEvent_t e_b0,
+                           cudaEvent_t e_b1) -> int {
+    int64_t launches = 0;
+    if (phase == 0) {
+      CU_TRY(cudaMemsetAsync(pool, 0, sizeof(float) * g.plane * planes_per_shot * Sb, c->stream));
+      if (e_f0) CU_TRY(cudaEventRecord(e_f0, c->stream));
+    }
 
     FwdParams fp{};
     fp.g = g;
@@ -279,28 +285,33 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     const bool boundary = adjoint && pl.store == HV_STORE_BOUNDARY;
     fp.s_shot_stride = full ? g.iplane * g.nt : 0;
     fp.ring_shot_stride = ringN * g.nt;
-    if (boundary) CU_TRY(cudaMemsetAsync(ring, 0, sizeof(float) * ringN * g.nt * Sb, c->stream));
+    if (boundary && phase == 0) CU_TRY(cudaMemsetAsync(ring, 0, sizeof(float) * ringN * g.nt * Sb, c->stream));
     const dim3 gridf(g.ntx, g.ntz, Gf);
-    for (int n = 0; n <= g.nt - 2; ++n) {
-      if (adjoint && pl.store == HV_STORE_CHECKPOINT && n % pl.k == 0) {
-        // save (u^n, u^{n-1}): both parity planes of slot 0, per shot; layout ckpt[S][nck][2][plane]
-        for (int s = 0; s < Sb; ++s)
-          CU_TRY(cudaMemcpyAsync(ckpt + ((size_t)s * pl.nck + n / pl.k) * 2 * g.plane,
-                                 pool + (size_t)s * planes_per_shot * g.plane, sizeof(float) * 2 * g.plane,
-                                 cudaMemcpyDeviceToDevice, c->stream));
+    if (phase == 0) {
+      for (int n = 0; n <= g.nt - 2; ++n) {
+        if (adjoint && pl.store == HV_STORE_CHECKPOINT && n % pl.k == 0) {
+          // save (u^n, u^{n-1}): both parity planes of slot 0, per shot; layout ckpt[S][nck][2][plane]
+          for (int s = 0; s < Sb; ++s)
+            CU_TRY(cudaMemcpyAsync(ckpt + ((size_t)s * pl.nck + n / pl.k) * 2 * g.plane,
+                                   pool + (size_t)s * planes_per_shot * g.plane, sizeof(float) * 2 * g.plane,
+                                   cudaMemcpyDeviceToDevice, c->stream));
+        }
+        fp.n = n;
+        fp.s_out = full ? store + (size_t)n * g.iplane : nullptr;
+        fp.ring_out = boundary ? ring + (size_t)(n + 1) * ringN : nullptr;
+        fwd_step_kernel<<<gridf, block, fwd_smem, c->stream>>>(map_halo, map_tile, map_q, fp);
+        launches++;
       }
-      fp.n = n;
-      fp.s_out = full ? store + (size_t)n * g.iplane : nullptr;
-      fp.ring_out = boundary ? ring + (size_t)(n + 1) * ringN : nullptr;
-      fwd_step_kernel<<<gridf, block, fwd_smem, c->stream>>>(map_halo, map_tile, map_q, fp);
-      launches++;
-    }
-    CU_TRY(cudaEventRecord(e_f1, c->stream));
-    {
-      const dim3 gg((g.nrec + 127) / 128, 1 + K, Sb);
-      gather_last_kernel<<<gg, 128, 0, c->stream>>>(g, pool, nslot, (g.nt - 1) & 1, fp.dbg_shot0, fp.d_bg, 0,
-                                                    dborn, 1, K, c->d_recI, c->d_recJ);
-      launches++;
+      if (e_f1) CU_TRY(cudaEventRecord(e_f1, c->stream));
+      {
+        const dim3 gg((g.nrec + 127) / 128, 1 + K, Sb);
+        gather_last_kernel<<<gg, 128, 0, c->stream>>>(g, pool, nslot, (g.nt - 1) & 1, fp.dbg_shot0, fp.d_bg, 0,
+                                                      dborn, 1, K, c->d_recI, c->d_recJ);
+        launches++;
+      }
+    CU_TRY(cudaGetLastError());
+    batch_launches = launches;
+    return HV_OK;
     }
     CU_TRY(cudaGetLastError());
     if (adjoint) {
@@ -338,7 +349,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
       bp.rec_I = c->d_recI;
       bp.rec_J = c->d_recJ;
       const dim3 gridb(g.ntx, g.ntz, Gb);
-      CU_TRY(cudaEventRecord(e_b0, c->stream));
+      if (e_b0) CU_TRY(cudaEventRecord(e_b0, c->stream));
       int cur_b = -1;
       for (int j = g.nt - 1; j >= 1; --j) {
         bp.j = j;
@@ -401,10 +412,67 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
         launches++;
       }
       CU_TRY(cudaGetLastError());
-    } else {
+    } else if (e_b0) {
       CU_TRY(cudaEventRecord(e_b0, c->stream));
     }
-    CU_TRY(cudaEventRecord(e_b1, c->stream));
+    if (e_b1) CU_TRY(cudaEventRecord(e_b1, c->stream));
+    batch_launches = launches;
+    return HV_OK;
+  };
+  const bool use_graphs = std::getenv("HV_NO_GRAPHS") == nullptr;
+  for (int b0 = 0; b0 < nloc; b0 += S) {
+    const int Sb = std::min(S, nloc - b0);
+    cudaEvent_t ev4[4];
+    for (int e = 0; e < 4; ++e)
+      if ((st = new_event(&ev4[e]))) return st;
+    if (!use_graphs) {
+      if ((st = enqueue_batch(0, b0, Sb, ev4[0], ev4[1], nullptr, nullptr))) return st;
+      launches += batch_launches;
+      if ((st = enqueue_batch(1, b0, Sb, nullptr, nullptr, ev4[2], ev4[3]))) return st;
+      launches += batch_launches;
+      continue;
+    }
+    for (int phase = 0; phase < 2; ++phase) {
+      char keybuf[1024];
+      std::snprintf(keybuf, sizeof keybuf,
+                    "ph%d w%d K%d S%d Sb%d b%d st%d k%d FG%d p%p W%p i%p Q%p db%p dg%p rr%p a%p s%p ck%p sg%p rg%p "
+                    "sb%p do%p od%p rc%p",
+                    phase, want, K, S, Sb, b0, pl.store, pl.k, FG, (void*)pool, (void*)W2, (void*)imgc, (void*)Q,
+                    (void*)dborn, (void*)dbg, (void*)rres, (void*)acc, (void*)store, (void*)ckpt, (void*)seg,
+                    (void*)ring, (void*)sbuf, (const void*)dobs, fwd ? o_d.dev : nullptr, (void*)rec_coef);
+      auto it = c->graphs.find(keybuf);
+      if (it == c->graphs.end()) {
+        if (c->graphs.size() >= 32) {
+          for (auto& kv : c->graphs) kv.second.destroy();
+          c->graphs.clear();
+        }
+        GraphEntry ge;
+        CU_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        const int s2 = enqueue_batch(phase, b0, Sb, nullptr, nullptr, nullptr, nullptr);
+        cudaGraph_t gr = nullptr;
+        const cudaError_t ec = cudaStreamEndCapture(c->stream, &gr);
+        if (s2 || ec != cudaSuccess) {
+          if (gr) cudaGraphDestroy(gr);
+          cudaGetLastError();
+          if (s2) return s2;
+          return fail(c, HV_ECUDA, std::string("stream capture: ") + cudaGetErrorString(ec));
+        }
+        const cudaError_t ei = cudaGraphInstantiate(&ge.exec, gr, 0);
+        cudaGraphDestroy(gr);
+        if (ei != cudaSuccess) {
+          cudaGetLastError();
+          return fail(c, HV_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ei));
+        }
+        ge.launches = batch_launches;
+        it = c->graphs.emplace(keybuf, ge).first;
+      }
+      // per-sweep timing events are recorded around the graph launches (events inside graphs cannot be timed)
+      CU_TRY(cudaEventRecord(ev4[2 * phase], c->stream));
+      CU_TRY(cudaGraphLaunch(it->second.exec, c->stream));
+      CU_TRY(cudaEventRecord(ev4[2 * phase + 1], c->stream));
+      launches += it->second.launches;
+      ++graph_launches;
+    }
   }
 
   // --- a8 (within the GPU): fixed-order sum over the shots in flight, into the caller's layout
@@ -425,10 +493,11 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   if (phi_user) CU_TRY(cudaMemcpyAsync(phi_user, phi_d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CU_TRY(cudaEventRecord(ev1, c->stream));
   CU_TRY(cudaStreamSynchronize(c->stream));
-  for (size_t i = 0; i + 3 < evs.size(); i += 4) {
+  const std::vector<cudaEvent_t>& tev = evs;
+  for (size_t i = 0; i + 3 < tev.size(); i += 4) {
     float a = 0, b = 0;
-    cudaEventElapsedTime(&a, evs[i], evs[i + 1]);
-    cudaEventElapsedTime(&b, evs[i + 2], evs[i + 3]);
+    cudaEventElapsedTime(&a, tev[i], tev[i + 1]);
+    cudaEventElapsedTime(&b, tev[i + 2], tev[i + 3]);
     ms_f += a;
     ms_b += b;
   }
@@ -439,7 +508,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   cudaEventDestroy(ev1);
   c->launches = launches;
   c->stats.kernel_launches = launches;
-  c->stats.graph_launches = 0;
+  c->stats.graph_launches = graph_launches;
   c->stats.shot_batch = S;
   c->stats.field_group = FG;
   c->stats.store = pl.store;
@@ -593,6 +662,7 @@ int hv_destroy(hv_ctx* c) {
   for (auto& kv : c->ws)
     if (kv.second.p) cudaFree(kv.second.p);
   for (auto& kv : c->fft_plans) cufftDestroy(kv.second);
+  for (auto& kv : c->graphs) kv.second.destroy();
   cudaFree(c->d_srcI);
   cudaFree(c->d_srcJ);
   cudaFree(c->d_recI);

@@ -14,6 +14,15 @@
 #include "hv_geo.h"
 
 namespace hvrt {
+// A captured sweep (forward or backward time loop of one shot batch).
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;
+  void destroy() {
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
+  }
+};
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -36,6 +45,7 @@ struct hv_ctx {
   // grow-only workspace
   std::map<std::string, hvrt::DevBuf> ws;
   std::map<std::tuple<int, int, int>, cufftHandle> fft_plans;  // (nz, nx, batch)
+  std::map<std::string, hvrt::GraphEntry> graphs;               // captured batch time loops
   std::string err = "";
   hv_stats stats{};
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;

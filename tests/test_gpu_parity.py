@@ -15,6 +15,7 @@ import workloads as W
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-4
+PHI_TOL = 2 * TOL   # phi = 1/2 |rho|^2 is quadratic in rho: rel(phi) ~ 2 rel_l2(rho)
 
 
 @pytest.fixture(scope="module")
@@ -67,7 +68,7 @@ def test_cfg0_gradient(hv, cfg0_ref):
     s = hv.Solver.from_workload(wl)
     phig, gg = s.gradient(m0, d_obs)
     assert rel_l2(gg, g) <= TOL, rel_l2(gg, g)
-    assert abs(phig - phi) <= TOL * phi
+    assert abs(phig - phi) <= PHI_TOL * phi
 
 
 def test_cfg0_gradient_near_zero_residual(hv, cfg0_ref):
@@ -94,7 +95,7 @@ def test_cfg0_fused_gradient_hessvec(hv, cfg0_ref):
     HV0 = pb.hessvec(list(V.astype(np.float64)))
     phig, gg, hvg = s.gradient_hessvec(m0, d_obs, V)
     assert rel_l2(gg, g) <= TOL and rel_l2(hvg, HV0) <= TOL
-    assert abs(phig - phi) <= TOL * phi
+    assert abs(phig - phi) <= PHI_TOL * phi
 
 
 # ---------------------------------------------------------------------------------------------- multi-tile
@@ -135,7 +136,7 @@ def test_ragged_forward_gradient(hv, ragged, store):
     s = hv.Solver.from_workload(wl, shot_batch=2, store=store)
     assert rel_l2(s.forward(wl.model), d) <= TOL
     phig, gg = s.gradient(m_start, d_obs)
-    assert rel_l2(gg, g) <= TOL and abs(phig - phi) <= TOL * phi
+    assert rel_l2(gg, g) <= TOL and abs(phig - phi) <= PHI_TOL * phi
 
 
 def test_ragged_shards_sum(hv, ragged):
@@ -263,15 +264,18 @@ def test_psido_apply_parity(hv, nz, nx, r):
 def test_cfg2_full_grid_fused_gradient_hessvec_slice(hv, store):
     wl = W.config(2).subset(shots=[31], nt=300)
     V = wl.probes([0, 1])
-    pb = wave.Problem(wl)
+    # R-grad: at nt = 300 only the direct wave in the water has arrived, identical for m and
+    # v_true, so the gradient is evaluated at a 4 % slow start model where the residual is O(|d|)
+    m0 = (0.96 * wl.model).astype(np.float32)
+    pb = wave.Problem(wl, m0)
     d_obs = wave.Problem(wl, wl.model_true).forward_all().astype(np.float32)
     phi, g = pb.gradient(d_obs, mode="checkpoint", ckpt=17)
     HV = pb.hessvec(list(V.astype(np.float64)), mode="checkpoint", ckpt=17)
     s = hv.Solver.from_workload(wl, store=store)
-    phig, gg, hvg = s.gradient_hessvec(wl.model, d_obs, V)
+    phig, gg, hvg = s.gradient_hessvec(m0, d_obs, V)
     assert rel_l2(gg, g) <= TOL, rel_l2(gg, g)
     assert rel_l2(hvg, HV) <= TOL, rel_l2(hvg, HV)
-    assert abs(phig - phi) <= TOL * phi
+    assert abs(phig - phi) <= PHI_TOL * phi
 
 
 def test_cfg3_full_grid_pdo_probe_slice(hv):

@@ -24,6 +24,8 @@
 #include "../../include/hv.h"
 #include "hv_internal.h"
 #include "hv_kernels.cuh"
+#include "hv_fwd2.cuh"
+#include "hv_bwd2.cuh"
 
 using namespace hvk;
 using namespace hvrt;
@@ -45,6 +47,8 @@ int make_tmap(hv_ctx* c, const float* base, long long nplanes, int box_w, int bo
   return HV_OK;
 }
 
+constexpr bool kTwoStepDefault = false;
+
 int grid1d(long long n) { return static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16)); }
 
 // ------------------------------------------------------------------------------------------ the plan
@@ -58,6 +62,7 @@ struct Plan {
   int S = 1;           // shots in flight
   int FG = 8;
   int nslot = 1;       // field slots per shot: 0 = background / residual adjoint, 1..K Born / adjoint, K+1 replay
+  int nlev = 2;        // pool planes per slot: 2 (parity, single-step kernels) or 4 (two-step forward, fwd2)
   int nacc = 0;        // accumulator slots
   double per_shot = 0; // bytes
 };
@@ -79,7 +84,7 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
   const double shared = F4 * (static_cast<double>(K) * g.plane * 2 + g.plane + g.iplane + 4.0 * K * g.nz * g.nx +
                               2.0 * g.nz * g.nx + (double)pl->nacc * g.plane) + (1 << 20);
   auto per_shot = [&](int store, int k) {
-    double b = F4 * 2.0 * pl->nslot * g.plane;                                  // field pool
+    double b = F4 * (store == HV_STORE_FULL ? 4.0 : 2.0) * pl->nslot * g.plane;  // field pool
     b += F4 * (double)K * g.nt * g.nrec;                                        // Born data
     if (grad) b += F4 * 2.0 * g.nt * g.nrec;                                    // data + residual
     if (adjoint) {
@@ -98,6 +103,10 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
   if (store != HV_STORE_FULL && store != HV_STORE_CHECKPOINT && store != HV_STORE_BOUNDARY)
     return fail(c, HV_EINVAL, "unknown storage mode " + std::to_string(store));
   pl->store = store;
+  // two-step kernels (fwd2 / bwd2) for FULL-store and forward-only calls; HV_T2=0 forces the single-step ones
+  const char* t2 = std::getenv("HV_T2");
+  const bool t2_on = t2 ? std::strcmp(t2, "0") != 0 : kTwoStepDefault;
+  pl->nlev = (store == HV_STORE_FULL && t2_on) ? 4 : 2;
   pl->k = k;
   pl->nck = (g.nt - 1 + k - 1) / k;
   pl->per_shot = per_shot(store, k);
@@ -108,7 +117,9 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
                                   " GB per shot in flight; budget " + std::to_string(budget / 1e9) + " GB");
   int S = c->cfg.shot_batch > 0 ? c->cfg.shot_batch : 0;
   const int ntiles = g.ntx * g.ntz;
-  pl->FG = std::min(FWD_FG_MAX, c->cfg.field_group > 0 ? c->cfg.field_group : 6);
+  // forward Born fields per unit (max; groups are near-equal): fewer groups = fewer background recomputes per
+  // shot and tile, more groups = finer load balance over the one-wave grid
+  pl->FG = std::min(FWD_FG_MAX, c->cfg.field_group > 0 ? c->cfg.field_group : 11);
   (void)ntiles;
   if (S <= 0) S = 32;  // every CTA loops over the batch's shots: more shots amortise q_k loads and imaging writes
   S = std::min(S, fit);
@@ -197,7 +208,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   float *pool, *dborn = nullptr, *dbg = nullptr, *rres = nullptr, *acc = nullptr, *store = nullptr,
                *ckpt = nullptr, *seg = nullptr, *ring = nullptr, *sbuf = nullptr;
   const long long ringN = ring_size(g);
-  const long long planes_per_shot = 2LL * nslot;
+  const long long planes_per_shot = static_cast<long long>(pl.nlev) * nslot;
+  const bool use_t2 = pl.nlev == 4;
   if ((st = ws_get(c, "pool", sizeof(float) * g.plane * planes_per_shot * S, (void**)&pool))) return st;
   if (K > 0 && (st = ws_get(c, "dborn", sizeof(float) * (size_t)S * K * g.nt * g.nrec, (void**)&dborn))) return st;
   if (grad) {
@@ -229,8 +241,21 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   const int Fb = (grad ? 1 : 0) + K;  // adjoint fields
   const int slot0_b = grad ? 0 : 1;
   const int Gb = std::max(1, (Fb + BWD_FG - 1) / BWD_FG);
-  const int fwd_smem = fwd_smem_bytes(K > 0 ? std::min(FG, K) : 0);
+  const int fwd_smem = fwd_smem_bytes(0);
   const dim3 block(BX, BY);
+  // Forward: one wave of CTAs (resident CTAs per SM x SMs) walking the shot-major unit list (hv_kernels.cuh).
+  // Backward: one CTA per (tile, group), each summing its imaging terms over all the batch's shots in registers
+  // (a single writer per accumulator address per launch).
+  auto fwd_grid = [&](long long units) -> int {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fwd_step_kernel, BX * BY, fwd_smem_bytes(0)) !=
+            cudaSuccess || nb < 1) {
+      cudaGetLastError();
+      nb = 1;
+    }
+    return static_cast<int>(std::max(1LL, std::min(static_cast<long long>(nb) * c->nsm, units)));
+  };
+  const long long ntiles_all = static_cast<long long>(g.ntx) * g.ntz;
   const dim3 tiles(g.ntx, g.ntz);
   double ms_f = 0, ms_b = 0;
   std::vector<cudaEvent_t> evs;
@@ -261,7 +286,6 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     fp.bg_update = 1;
     fp.born_slot0 = 1;
     fp.K = K;
-    fp.FG = FG;
     fp.S = Sb;
     fp.W2 = W2;
     fp.imgc = imgc;
@@ -286,8 +310,47 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     fp.s_shot_stride = full ? g.iplane * g.nt : 0;
     fp.ring_shot_stride = ringN * g.nt;
     if (boundary && phase == 0) CU_TRY(cudaMemsetAsync(ring, 0, sizeof(float) * ringN * g.nt * Sb, c->stream));
-    const dim3 gridf(g.ntx, g.ntz, Gf);
-    if (phase == 0) {
+    fp.G = Gf;
+    const dim3 gridf(fwd_grid(ntiles_all * Gf * Sb));
+    if (phase == 0 && use_t2) {
+      Fwd2Params f2{};
+      f2.g = g;
+      f2.nslot = nslot;
+      f2.pool = pool;
+      f2.born_slot0 = 1;
+      f2.K = K;
+      f2.S = Sb;
+      f2.G = Gf;
+      f2.W2 = W2;
+      f2.imgc = imgc;
+      f2.s_shot_stride = fp.s_shot_stride;
+      f2.shot0 = b0;
+      f2.src_I = c->d_srcI;
+      f2.src_J = c->d_srcJ;
+      f2.src_amp = c->d_src_amp;
+      f2.trec_beg = c->d_trec2_beg;
+      f2.trec_id = c->d_trec2_id;
+      f2.rec_I = c->d_recI;
+      f2.rec_J = c->d_recJ;
+      f2.d_bg = fp.d_bg;
+      f2.dbg_shot0 = fp.dbg_shot0;
+      f2.d_born = dborn;
+      int nb = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fwd2_kernel, BX * BY, F2_SMEM_BYTES) != cudaSuccess ||
+          nb < 1) {
+        cudaGetLastError();
+        nb = 1;
+      }
+      const long long units = static_cast<long long>(g.ntx2) * g.ntz2 * Gf * Sb;
+      const dim3 grid2(static_cast<unsigned>(std::max(1LL, std::min(static_cast<long long>(nb) * c->nsm, units))));
+      for (int n = 0; n <= g.nt - 2; n += 2) {
+        f2.n = n;
+        f2.two = n + 2 <= g.nt - 1;
+        f2.s_out = full ? store + (size_t)n * g.iplane : nullptr;
+        fwd2_kernel<<<grid2, block, F2_SMEM_BYTES, c->stream>>>(map_halo, map_tile, map_q, f2);
+        launches++;
+      }
+    } else if (phase == 0) {
       for (int n = 0; n <= g.nt - 2; ++n) {
         if (adjoint && pl.store == HV_STORE_CHECKPOINT && n % pl.k == 0) {
           // save (u^n, u^{n-1}): both parity planes of slot 0, per shot; layout ckpt[S][nck][2][plane]
@@ -302,10 +365,13 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
         fwd_step_kernel<<<gridf, block, fwd_smem, c->stream>>>(map_halo, map_tile, map_q, fp);
         launches++;
       }
+    }
+    if (phase == 0) {
       if (e_f1) CU_TRY(cudaEventRecord(e_f1, c->stream));
       {
         const dim3 gg((g.nrec + 127) / 128, 1 + K, Sb);
-        gather_last_kernel<<<gg, 128, 0, c->stream>>>(g, pool, nslot, (g.nt - 1) & 1, fp.dbg_shot0, fp.d_bg, 0,
+        gather_last_kernel<<<gg, 128, 0, c->stream>>>(g, pool, nslot, pl.nlev, (g.nt - 1) & (pl.nlev - 1),
+                                                      fp.dbg_shot0, fp.d_bg, 0,
                                                       dborn, 1, K, c->d_recI, c->d_recJ);
         launches++;
       }
@@ -335,6 +401,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
       bp.g = g;
       bp.pool = pool;
       bp.nslot = nslot;
+      bp.nlev = pl.nlev;
       bp.slot0 = slot0_b;
       bp.F = Fb;
       bp.S = Sb;
@@ -351,7 +418,40 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
       const dim3 gridb(g.ntx, g.ntz, Gb);
       if (e_b0) CU_TRY(cudaEventRecord(e_b0, c->stream));
       int cur_b = -1;
-      for (int j = g.nt - 1; j >= 1; --j) {
+      int j_t1 = g.nt - 1;  // first level left for the single-step kernel
+      if (use_t2) {         // FULL store: two levels per launch, j = nt-1, nt-3, ... >= 2
+        Bwd2Params b2{};
+        b2.g = g;
+        b2.nslot = nslot;
+        b2.pool = pool;
+        b2.slot0 = slot0_b;
+        b2.F = Fb;
+        b2.S = Sb;
+        b2.W2 = W2;
+        b2.s_shot_stride = g.iplane * g.nt;
+        b2.acc = acc;
+        b2.rho_res = rres;
+        b2.rho_born = dborn;
+        b2.Kb = K;
+        b2.rec_coef = rec_coef;
+        b2.trec_beg = c->d_trec2_beg;
+        b2.trec_id = c->d_trec2_id;
+        b2.trecx_beg = c->d_trecx_beg;
+        b2.trecx_id = c->d_trecx_id;
+        b2.rec_I = c->d_recI;
+        b2.rec_J = c->d_recJ;
+        const dim3 grid2(g.ntx2, g.ntz2, Gb);
+        int j = g.nt - 1;
+        for (; j >= 2; j -= 2) {
+          b2.j = j;
+          b2.img_top = j <= g.nt - 2;
+          b2.s_lvl = store + (size_t)j * g.iplane;
+          bwd2_kernel<<<grid2, block, B2_SMEM_BYTES, c->stream>>>(map_halo, map_tile, b2);
+          launches++;
+        }
+        j_t1 = j;  // 1 (one level left: imaging only) or 0
+      }
+      for (int j = j_t1; j >= 1; --j) {
         bp.j = j;
         bp.update = j >= 2;
         bp.imaging = j <= g.nt - 2;
@@ -395,7 +495,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
               rp.d_bg = nullptr;
               rp.d_born = nullptr;
               rp.s_shot_stride = g.iplane * pl.k;
-              const dim3 gridr(g.ntx, g.ntz, 1);
+              rp.G = 1;
+              const dim3 gridr(fwd_grid(ntiles_all * Sb));
               for (int n = b; n < e; ++n) {
                 rp.n = n;
                 rp.s_out = seg + (size_t)(n - b) * g.iplane;
@@ -568,6 +669,7 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
   cudaDeviceProp prop{};
   if (cudaGetDeviceProperties(&prop, k.device) != cudaSuccess || prop.major < 10)
     return bad(HV_ECUDA, "device is not sm_100-class");
+  c->nsm = prop.multiProcessorCount;
   if (cudaSetDevice(k.device) != cudaSuccess) return bad(HV_ECUDA, "cudaSetDevice failed");
 
   // geometry
@@ -579,7 +681,9 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
   g.Nx = k.nx + 2 * k.sponge;
   g.ntx = (g.Nx + TX - 1) / TX;
   g.ntz = (g.Nz + TZ - 1) / TZ;
-  g.P = g.ntx * TX;
+  g.ntx2 = (g.Nx + OX - 1) / OX;
+  g.ntz2 = (g.Nz + OZ - 1) / OZ;
+  g.P = std::max(g.ntx * TX, (g.ntx2 * OX + 3) / 4 * 4);
   g.c0 = (g.W / 4) * 4;
   g.PI = ((g.W + g.nx - g.c0) + 3) / 4 * 4;
   g.plane = (long long)g.Nz * g.P;
@@ -607,6 +711,24 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
     std::vector<int> fillp(beg.begin(), beg.end() - 1);
     for (int i = 0; i < k.nrec; ++i) ids[fillp[(rI[i] / TZ) * g.ntx + rJ[i] / TX]++] = i;
   }
+  // receivers owned by each output tile of the two-step forward kernel
+  const int ntiles2 = g.ntx2 * g.ntz2;
+  std::vector<int> beg2(ntiles2 + 1, 0), ids2(k.nrec);
+  for (int i = 0; i < k.nrec; ++i) beg2[(rI[i] / OZ) * g.ntx2 + rJ[i] / OX + 1]++;
+  for (int t = 0; t < ntiles2; ++t) beg2[t + 1] += beg2[t];
+  {
+    std::vector<int> fillp(beg2.begin(), beg2.end() - 1);
+    for (int i = 0; i < k.nrec; ++i) ids2[fillp[(rI[i] / OZ) * g.ntx2 + rJ[i] / OX]++] = i;
+  }
+  // receivers inside each two-step tile's ext region (core + R cells): level-j injection of the two-step adjoint
+  std::vector<int> begx(ntiles2 + 1, 0), idsx;
+  for (int t = 0; t < ntiles2; ++t) {
+    const int tz = t / g.ntx2, txx = t % g.ntx2;
+    const int z0 = tz * OZ - R, x0 = txx * OX - R;
+    for (int i = 0; i < k.nrec; ++i)
+      if (rI[i] >= z0 && rI[i] < z0 + TZ && rJ[i] >= x0 && rJ[i] < x0 + TX) idsx.push_back(i);
+    begx[t + 1] = static_cast<int>(idsx.size());
+  }
   std::vector<float> amp(k.nt);
   for (int n = 0; n < k.nt; ++n)
     amp[n] = static_cast<float>((double)k.dt * k.dt * (double)c->wavelet[n] / ((double)k.h * k.h));
@@ -620,6 +742,10 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
       !up((void**)&c->d_recJ, rJ.data(), sizeof(int) * rJ.size()) ||
       !up((void**)&c->d_trec_beg, beg.data(), sizeof(int) * beg.size()) ||
       !up((void**)&c->d_trec_id, ids.data(), sizeof(int) * ids.size()) ||
+      !up((void**)&c->d_trec2_beg, beg2.data(), sizeof(int) * beg2.size()) ||
+      !up((void**)&c->d_trec2_id, ids2.data(), sizeof(int) * ids2.size()) ||
+      !up((void**)&c->d_trecx_beg, begx.data(), sizeof(int) * begx.size()) ||
+      !up((void**)&c->d_trecx_id, idsx.data(), sizeof(int) * std::max<size_t>(1, idsx.size())) ||
       !up((void**)&c->d_src_amp, amp.data(), sizeof(float) * amp.size())) {
     cudaGetLastError();
     hv_destroy(c);
@@ -646,6 +772,8 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
           cudaSuccess ||
       cudaFuncSetAttribute(bwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_BYTES) !=
           cudaSuccess ||
+      cudaFuncSetAttribute(fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, F2_SMEM_BYTES) != cudaSuccess ||
+      cudaFuncSetAttribute(bwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, B2_SMEM_BYTES) != cudaSuccess ||
       cudaFuncSetAttribute(rev_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_BYTES) !=
           cudaSuccess) {
     cudaGetLastError();
@@ -669,6 +797,10 @@ int hv_destroy(hv_ctx* c) {
   cudaFree(c->d_recJ);
   cudaFree(c->d_trec_beg);
   cudaFree(c->d_trec_id);
+  cudaFree(c->d_trec2_beg);
+  cudaFree(c->d_trec2_id);
+  cudaFree(c->d_trecx_beg);
+  cudaFree(c->d_trecx_id);
   cudaFree(c->d_src_amp);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;

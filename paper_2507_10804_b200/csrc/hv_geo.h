@@ -27,12 +27,19 @@ constexpr int NSTAGE = HV_NSTAGE;             // TMA pipeline depth (items in fl
 constexpr int STAGE_FLOATS = TILE_FLOATS + PT_FLOATS;
 constexpr int STAGES_BYTES = NSTAGE * STAGE_FLOATS * 4;
 constexpr int BAR_BYTES = 128;              // keeps the q tiles behind the barriers 128-byte aligned (TMA)
-// forward CTA: stages + the q_k tiles of its field group (loaded once, reused by every shot of the batch)
-constexpr int FWD_FG_MAX = 16;
-constexpr int fwd_smem_bytes(int fg) { return STAGES_BYTES + BAR_BYTES + fg * PT_BYTES; }
+// forward CTA: NSTAGE_F stages of halo u^n + tile u^{n-1} + tile q_k
+#ifndef HV_NSTAGE_F
+#define HV_NSTAGE_F 4
+#endif
+constexpr int NSTAGE_F = HV_NSTAGE_F;
+constexpr int FSTAGE_FLOATS = TILE_FLOATS + 2 * PT_FLOATS;
+constexpr int FSTAGES_BYTES = NSTAGE_F * FSTAGE_FLOATS * 4;
+constexpr int FWD_FG_MAX = 64;
+constexpr int fwd_smem_bytes(int) { return FSTAGES_BYTES + BAR_BYTES; }
 // backward CTA: stages; its BWD_FG adjoint fields keep their imaging sums over the batch's shots in registers
 constexpr int BWD_FG = HV_BWD_FG;
 constexpr int BWD_SMEM_BYTES = STAGES_BYTES + BAR_BYTES;
+constexpr int B2_SMEM_BYTES = STAGES_BYTES + PT_FLOATS * 4 + BAR_BYTES;  // two-step adjoint: + mid
 
 // standard 8th-order central second-derivative weights (unscaled; h^-2 is folded into the coefficients)
 #define HV_A0 (-205.0f / 72.0f)
@@ -41,12 +48,23 @@ constexpr int BWD_SMEM_BYTES = STAGES_BYTES + BAR_BYTES;
 #define HV_A3 (8.0f / 315.0f)
 #define HV_A4 (-1.0f / 560.0f)
 
+// two-step forward kernel (hv_fwd2.cuh): the TX x TZ region is computed at level n+1, its OX x OZ core at n+2
+constexpr int OX = TX - 2 * R;
+constexpr int OZ = TZ - 2 * R;
+#ifndef HV_NSTAGE_F2
+#define HV_NSTAGE_F2 3
+#endif
+constexpr int NSTAGE_F2 = HV_NSTAGE_F2;
+constexpr int F2_SMEM_BYTES = NSTAGE_F2 * FSTAGE_FLOATS * 4 + PT_FLOATS * 4 + BAR_BYTES;
+
+
 struct Geo {
   int nz, nx, W;        // interior grid, sponge width
   int Nz, Nx;           // padded grid
-  int P;                // row pitch of padded planes (floats) = ntx * TX
+  int P;                // row pitch of padded planes (floats) >= ntx * TX and >= ntx2 * OX
   int PI, c0;           // interior-store row pitch and first padded column stored (c0 % 4 == 0)
-  int ntx, ntz;         // tile grid
+  int ntx, ntz;         // tile grid (TX x TZ tiles: single-step kernels)
+  int ntx2, ntz2;       // tile grid of the two-step forward kernel (OX x OZ output tiles)
   long long plane;      // Nz * P
   long long iplane;     // nz * PI
   float kc;             // eta_max * dt / (2 W^2): c = kc (d_z^2 + d_x^2)

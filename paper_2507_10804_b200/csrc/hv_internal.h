@@ -35,12 +35,15 @@ struct hv_ctx {
   std::vector<float> wavelet;
   int nloc = 0;  // shots in this rank's shard
   int dev = 0;
+  int nsm = 148;  // SMs of the device (grid sizing)
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   hvk::Geo g{};
   // persistent device arrays
   int *d_srcI = nullptr, *d_srcJ = nullptr, *d_recI = nullptr, *d_recJ = nullptr;
   int *d_trec_beg = nullptr, *d_trec_id = nullptr;
+  int *d_trec2_beg = nullptr, *d_trec2_id = nullptr;  // per output (core) tile of the two-step kernels
+  int *d_trecx_beg = nullptr, *d_trecx_id = nullptr;  // per ext region (core + R) of the two-step kernels
   float* d_src_amp = nullptr;
   // grow-only workspace
   std::map<std::string, hvrt::DevBuf> ws;

@@ -52,8 +52,21 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Waits for the phase; a pipeline bug that would hang the GPU traps instead after ~2^34 cycles (~9 s), so the
+// call fails with a CUDA error rather than wedging the device.
+#ifndef HV_WAIT_GUARD
+#define HV_WAIT_GUARD 1
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if !HV_WAIT_GUARD
   while (!mbar_try_wait(bar, parity)) {
+  }
+  return;
+#endif
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity)) {
+    if (clock64() - t0 > (1LL << 34)) __trap();
   }
 }
 __device__ __forceinline__ void tma_load_3d(float* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
@@ -63,6 +76,26 @@ __device__ __forceinline__ void tma_load_3d(float* dst, const CUtensorMap* map, 
       "[%5];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
+}
+// Same, with an L2 eviction-priority hint (a policy from createpolicy): q_k tiles are re-read by every shot and
+// are loaded evict_last so they stay L2-resident; single-use pointwise tiles go evict_first.
+__device__ __forceinline__ void tma_load_3d_hint(float* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                                 int z, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -75,32 +108,68 @@ __device__ __forceinline__ float f4(const float4& v, int i) {
   return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
 }
 
-// Unscaled 8th-order Laplacian of this thread's RZ x 4 points from a halo tile in shared memory.
-// Thread (tx, ty) owns tile rows ty*RZ .. ty*RZ+RZ-1 and columns 4tx .. 4tx+3.
-__device__ __forceinline__ void lap_points(const float* __restrict__ t, int tx, int ty, float (&L)[RZ][4],
-                                           float (&C)[RZ][4]) {
+// Paired fp32 arithmetic (sm_100 FADD2 / FMUL2 / FFMA2: two lanes per instruction, each lane rounded exactly
+// like the scalar FADD / FMUL / FFMA, so results are bit-identical to the scalar formulation).
+#ifndef HV_PAIRED
+#define HV_PAIRED 1
+#endif
+#if HV_PAIRED
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+// a - b as one FFMA2 (-1 * b + a is exact before the single rounding, so it equals FADD(a, -b))
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __ffma2_rn(b, make_float2(-1.0f, -1.0f), a); }
+#else  // scalar lanes (same roundings)
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y)); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  return make_float2(__fmaf_rn(a.x, b.x, c.x), __fmaf_rn(a.y, b.y, c.y));
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y)); }
+#endif
+__device__ __forceinline__ float2 splat2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
+__device__ __forceinline__ float2 half2of(const float4& v, int h) { return h == 0 ? lo2(v) : hi2(v); }
+
+// Unscaled 8th-order Laplacian of this thread's RZ x 4 points from a halo tile in shared memory, as column pairs
+// (h = 0: columns 0-1, h = 1: columns 2-3). Thread (tx, ty) owns tile rows ty*RZ .. ty*RZ+RZ-1 and columns
+// 4tx .. 4tx+3. Per point: s = A1 (x+-1 + z+-1) + A2 (..2) + A3 (..3) + A4 (..4), L = 2 A0 ctr + s, with the
+// pair sums (x-pair) + (z-pair) in that order.
+// t points at element (0, 0) of a buffer of row width W whose element (ty*RZ + r + R, 4tx + i + R) is the
+// stencil centre of the thread's point (r, i) (W = HX: a staged halo tile).
+template <int W>
+__device__ __forceinline__ void lap_points_w(const float* __restrict__ t, int tx, int ty, float2 (&L)[RZ][2],
+                                             float2 (&C)[RZ][2]) {
   const int col = R + tx * 4;
   float4 zw[RZ + 2 * R];
 #pragma unroll
-  for (int k = 0; k < RZ + 2 * R; ++k) zw[k] = ld4(t + (ty * RZ + k) * HX + col);
+  for (int k = 0; k < RZ + 2 * R; ++k) zw[k] = ld4(t + (ty * RZ + k) * W + col);
 #pragma unroll
   for (int r = 0; r < RZ; ++r) {
-    const float* row = t + (ty * RZ + r + R) * HX + tx * 4;
+    const float* row = t + (ty * RZ + r + R) * W + tx * 4;
     const float4 a = ld4(row);
     const float4 b = zw[r + R];
     const float4 c = ld4(row + 8);
     const float xs[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float ctr = xs[4 + i];
-      float s = HV_A1 * ((xs[3 + i] + xs[5 + i]) + (f4(zw[r + 3], i) + f4(zw[r + 5], i)));
-      s = fmaf(HV_A2, (xs[2 + i] + xs[6 + i]) + (f4(zw[r + 2], i) + f4(zw[r + 6], i)), s);
-      s = fmaf(HV_A3, (xs[1 + i] + xs[7 + i]) + (f4(zw[r + 1], i) + f4(zw[r + 7], i)), s);
-      s = fmaf(HV_A4, (xs[0 + i] + xs[8 + i]) + (f4(zw[r + 0], i) + f4(zw[r + 8], i)), s);
-      L[r][i] = fmaf(2.0f * HV_A0, ctr, s);
-      C[r][i] = ctr;
+    for (int h = 0; h < 2; ++h) {
+      const int i = 2 * h;
+      auto P = [&](int k) { return make_float2(xs[k + i], xs[k + i + 1]); };
+      auto Z = [&](int k) { return half2of(zw[r + k], h); };
+      const float2 ctr = P(4);
+      float2 s = mul2(splat2(HV_A1), add2(add2(P(3), P(5)), add2(Z(3), Z(5))));
+      s = fma2(splat2(HV_A2), add2(add2(P(2), P(6)), add2(Z(2), Z(6))), s);
+      s = fma2(splat2(HV_A3), add2(add2(P(1), P(7)), add2(Z(1), Z(7))), s);
+      s = fma2(splat2(HV_A4), add2(add2(P(0), P(8)), add2(Z(0), Z(8))), s);
+      L[r][h] = fma2(splat2(2.0f * HV_A0), ctr, s);
+      C[r][h] = ctr;
     }
   }
+}
+__device__ __forceinline__ void lap_points(const float* __restrict__ t, int tx, int ty, float2 (&L)[RZ][2],
+                                           float2 (&C)[RZ][2]) {
+  lap_points_w<HX>(t, tx, ty, L, C);
 }
 
 // Sponge coefficient c = kc (d_z^2 + d_x^2), d_z = max(0, W - I, I - (W + nz - 1)) (C10).
@@ -130,6 +199,7 @@ __host__ __device__ __forceinline__ int ring_size(const Geo& g) { return 2 * R *
 
 // ------------------------------------------------------------------------------------------------ forward
 
+
 struct FwdParams {
   Geo g;
   int nslot;              // pool plane index = ((s_local * nslot) + slot) * 2 + parity
@@ -139,8 +209,8 @@ struct FwdParams {
   int bg_update;          // write u^{n+1}? (1; 0 = sampling-only use)
   int born_slot0;         // Born field k lives in slot born_slot0 + k
   int K;                  // Born fields
-  int FG;                 // Born fields per CTA (grid.z = field groups; every CTA loops over the S shots)
   int S;                  // shots of the batch
+  int G;                  // Born-field groups (near-equal sizes, group_begin); work unit = (shot, group, tile)
   const float* W2;        // [Nz][P]   dt^2 v^2 / h^2 (0 outside the padded grid)
   const float* imgc;      // [nz][PI]  2 dt^2 / (v h^2); with s_out: store s^n = imgc * Lu^n
   float* s_out;           // level-n slot of the imaging-factor store for s_local = 0, or null
@@ -160,60 +230,44 @@ struct FwdParams {
   long long ring_shot_stride;
 };
 
-// Per-point damping of this thread's points (SP: the tile touches the sponge): (1 - c) and 1 / (1 + c).
+// Per-point damping of this thread's points (SP: the tile touches the sponge): (1 - c) and 1 / (1 + c), as
+// column pairs h = 0 (columns 0-1), h = 1 (columns 2-3).
 template <bool SP>
 struct Damp {
-  float cm[RZ][4], ci_[RZ][4];
+  float2 cm[RZ][2], ci_[RZ][2];
   __device__ __forceinline__ void init(const Geo& g, int I0, int J0) {
 #pragma unroll
     for (int r = 0; r < RZ; ++r)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float c = sponge_c(g, I0 + r, J0 + i);
-        cm[r][i] = 1.0f - c;
-        ci_[r][i] = 1.0f / (1.0f + c);
+      for (int h = 0; h < 2; ++h) {
+        const float c0 = sponge_c(g, I0 + r, J0 + 2 * h), c1 = sponge_c(g, I0 + r, J0 + 2 * h + 1);
+        cm[r][h] = make_float2(1.0f - c0, 1.0f - c1);
+        ci_[r][h] = make_float2(1.0f / (1.0f + c0), 1.0f / (1.0f + c1));
       }
   }
-  __device__ __forceinline__ float ci(int r, int i) const { return ci_[r][i]; }
+  __device__ __forceinline__ float ci(int r, int i) const { return (i & 1) ? ci_[r][i >> 1].y : ci_[r][i >> 1].x; }
   // [2 C - (1 - c) prev + rhs] / (1 + c)
-  __device__ __forceinline__ float upd(int r, int i, float C, float prev, float rhs) const {
-    return (fmaf(2.0f, C, rhs) - cm[r][i] * prev) * ci_[r][i];
+  __device__ __forceinline__ float2 upd(int r, int h, float2 C, float2 prev, float2 rhs) const {
+    const float2 t = fma2(splat2(2.0f), C, rhs);
+    return mul2(fma2(make_float2(-cm[r][h].x, -cm[r][h].y), prev, t), ci_[r][h]);
+  }
+  __device__ __forceinline__ float upd1(int r, int i, float C, float prev, float rhs) const {
+    const float cmi = (i & 1) ? cm[r][i >> 1].y : cm[r][i >> 1].x;
+    return (fmaf(2.0f, C, rhs) - cmi * prev) * ci(r, i);
   }
 };
-// Register-lean variant (backward kernel, which also holds BWD_FG imaging sums): keeps c only and recomputes
-// 1 / (1 + c) correctly rounded (__frcp_rn == 1.0f / (1.0f + c), so both variants give identical bits).
-template <bool SP>
-struct DampLite {
-  float c[RZ][4];
-  __device__ __forceinline__ void init(const Geo& g, int I0, int J0) {
-#pragma unroll
-    for (int r = 0; r < RZ; ++r)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) c[r][i] = sponge_c(g, I0 + r, J0 + i);
-  }
-  __device__ __forceinline__ float upd(int r, int i, float C, float prev, float rhs) const {
-    return (fmaf(2.0f, C, rhs) - (1.0f - c[r][i]) * prev) * __frcp_rn(1.0f + c[r][i]);
-  }
-};
-template <>
-struct DampLite<false> {
-  __device__ __forceinline__ void init(const Geo&, int, int) {}
-  __device__ __forceinline__ float upd(int, int, float C, float prev, float rhs) const {
-    return fmaf(2.0f, C, rhs) - prev;
-  }
-};
-#ifndef HV_BWD_LITE
-#define HV_BWD_LITE 0
-#endif
-template <bool SP>
-using BwdDamp = typename std::conditional<HV_BWD_LITE != 0, DampLite<SP>, Damp<SP>>::type;
 template <>
 struct Damp<false> {
   __device__ __forceinline__ void init(const Geo&, int, int) {}
-  __device__ __forceinline__ float upd(int, int, float C, float prev, float rhs) const {
+  __device__ __forceinline__ float2 upd(int, int, float2 C, float2 prev, float2 rhs) const {
+    return sub2(fma2(splat2(2.0f), C, rhs), prev);
+  }
+  __device__ __forceinline__ float upd1(int, int, float C, float prev, float rhs) const {
     return fmaf(2.0f, C, rhs) - prev;
   }
 };
+template <bool SP>
+using BwdDamp = Damp<SP>;
 
 template <bool SP>
 __device__ __forceinline__ float dmp_ci(const Damp<SP>& d, int r, int i) {
@@ -221,86 +275,126 @@ __device__ __forceinline__ float dmp_ci(const Damp<SP>& d, int r, int i) {
   else return 1.0f;
 }
 
-// Consumer/producer bookkeeping of the NSTAGE-deep TMA ring (no divisions in the item loop).
-struct Ring {
+// Consumer/producer bookkeeping of an N-deep TMA ring (no divisions in the item loop).
+template <int N>
+struct RingN {
   int stage = 0;
   uint32_t phase = 0;
   __device__ __forceinline__ void advance() {
-    if (++stage == NSTAGE) {
+    if (++stage == N) {
       stage = 0;
       phase ^= 1u;
     }
   }
 };
+using Ring = RingN<NSTAGE>;     // backward / reverse kernels
+using RingF = RingN<NSTAGE_F>;  // forward kernel
+
+// Forward schedule (v4). Work unit = (shot s, field group grp, tile): the background item of shot s on the tile
+// (its Laplacian L u^n feeds the group's Born sources) followed by the group's nf Born items. Units are numbered
+// shot-major (s, grp, tile) and CTA c of n takes units c, c + n, c + 2n, ...: every launch is one balanced wave
+// (no partial last wave), and at any moment the resident CTAs work on the same shot, so halo overlaps between
+// neighbouring tiles and the background tile shared by the groups are L2 hits. Each item's q_k tile travels in
+// its pipeline stage (q stays L2-resident across shots), so the TMA ring runs across unit boundaries.
+#ifndef HV_L2_HINTS
+#define HV_L2_HINTS 1
+#endif
+// Born fields of forward group grp: [group_begin(grp), group_begin(grp + 1)), G near-equal groups.
+__device__ __forceinline__ int group_begin(int K, int G, int grp) { return (K * grp) / G; }
+
+struct FwdProducer {  // thread 0's walk over this CTA's items (decoded once per unit: no divisions per item)
+  const CUtensorMap *mh, *mt, *mq;
+  float* stages;
+  uint64_t* bars;
+  int u, t;                 // current unit, next item within it (0 = background, 1..nf = Born fields)
+  int U, nstep, ntl;
+  int x0, z0, pl_bg, pl_born, fb, nf;  // decoded unit
+  bool upd;
+  uint64_t pol_first, pol_last;
+  RingF ring;
+  __device__ __forceinline__ void decode(const FwdParams& p) {
+    if (u >= U) return;
+    const int s = u / (p.G * ntl);
+    const int rem = u - s * p.G * ntl;
+    const int grp = rem / ntl, tile = rem - grp * ntl;
+    const int by = tile / p.g.ntx;
+    x0 = (tile - by * p.g.ntx) * TX, z0 = by * TZ;
+    fb = group_begin(p.K, p.G, grp);
+    nf = group_begin(p.K, p.G, grp + 1) - fb;
+    upd = grp == 0 && p.bg_update;
+    pl_bg = (s * p.nslot + p.bg_slot) * 2;
+    pl_born = (s * p.nslot + p.born_slot0 + fb) * 2;
+  }
+  __device__ __forceinline__ void issue(const FwdParams& p) {
+    if (u >= U) return;
+    const int par_n = p.n & 1, par_new = par_n ^ 1;
+    float* st = stages + ring.stage * FSTAGE_FLOATS;
+    uint64_t* bar = &bars[ring.stage];
+    if (t == 0) {
+      mbar_expect_tx(bar, TILE_BYTES + (upd ? PT_BYTES : 0));
+      tma_load_3d(st, mh, bar, x0 - R, z0 - R, pl_bg + par_n);
+#if HV_L2_HINTS
+      if (upd) tma_load_3d_hint(st + TILE_FLOATS, mt, bar, x0, z0, pl_bg + par_new, pol_first);
+#else
+      if (upd) tma_load_3d(st + TILE_FLOATS, mt, bar, x0, z0, pl_bg + par_new);
+#endif
+    } else {
+      const int pl = pl_born + 2 * (t - 1);
+      mbar_expect_tx(bar, TILE_BYTES + 2 * PT_BYTES);
+      tma_load_3d(st, mh, bar, x0 - R, z0 - R, pl + par_n);
+#if HV_L2_HINTS
+      tma_load_3d_hint(st + TILE_FLOATS, mt, bar, x0, z0, pl + par_new, pol_first);
+      tma_load_3d_hint(st + TILE_FLOATS + PT_FLOATS, mq, bar, x0, z0, fb + t - 1, pol_last);
+#else
+      tma_load_3d(st + TILE_FLOATS, mt, bar, x0, z0, pl + par_new);
+      tma_load_3d(st + TILE_FLOATS + PT_FLOATS, mq, bar, x0, z0, fb + t - 1);
+#endif
+    }
+    ring.advance();
+    if (++t > nf) {
+      t = 0;
+      u += nstep;
+      decode(p);
+    }
+  }
+};
 
 template <bool SP>
-__device__ __forceinline__ void fwd_body(const CUtensorMap* mh, const CUtensorMap* mt, const CUtensorMap* mq,
-                                         const FwdParams& p, float* stages, float* qs, uint64_t* bars) {
+__device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages, uint64_t* bars, int s, int grp,
+                                         int bx, int by, RingF& cons, FwdProducer& prod) {
   const Geo& g = p.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
-  const int x0 = blockIdx.x * TX, z0 = blockIdx.y * TZ;
-  const int grp = blockIdx.z;
-  const int fb = grp * p.FG;
-  const int nf = max(0, min(p.K, fb + p.FG) - fb);   // Born fields of this CTA
-  const int nitems = p.S * (1 + nf);                  // per shot: background, then its Born fields
+  const int x0 = bx * TX, z0 = by * TZ;
+  const int fb = group_begin(p.K, p.G, grp);
+  const int nf = group_begin(p.K, p.G, grp + 1) - fb;
   const int par_n = p.n & 1, par_new = par_n ^ 1;
   const bool leader = (grp == 0) && p.bg_update;
-  uint64_t* qbar = bars + NSTAGE;
-
-  // producer (thread 0): next item (ps, pt) -> stage
-  int ps = 0, pt = 0, issued = 0;
-  Ring prod;
-  auto issue_next = [&]() {
-    float* st = stages + prod.stage * STAGE_FLOATS;
-    const bool upd = pt > 0 || leader;
-    const int slot = pt == 0 ? p.bg_slot : p.born_slot0 + fb + pt - 1;
-    const int pl = (ps * p.nslot + slot) * 2;
-    mbar_expect_tx(&bars[prod.stage], TILE_BYTES + (upd ? PT_BYTES : 0));
-    tma_load_3d(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_n);
-    if (upd) tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_new);
-    prod.advance();
-    if (++pt > nf) {
-      pt = 0;
-      ++ps;
-    }
-    ++issued;
-  };
-  if (tid == 0) {
-    if (nf > 0) {  // q_k tiles of the group, once for all shots
-      mbar_expect_tx(qbar, nf * PT_BYTES);
-      for (int t = 0; t < nf; ++t) tma_load_3d(qs + t * PT_FLOATS, mq, qbar, x0, z0, fb + t);
-    }
-    while (issued < min(NSTAGE, nitems)) issue_next();
-  }
 
   const int I0 = z0 + ty * RZ;
   const int J0 = x0 + tx * 4;
   const int so = ty * RZ * TX + tx * 4;                       // smem offset of this thread's first point
   const long long go = static_cast<long long>(I0) * g.P + J0;  // plane offset of this thread's first point
-  float w[RZ][4];
+  float2 w[RZ][2];
 #pragma unroll
   for (int r = 0; r < RZ; ++r) {
     const float4 wv = ldg4(p.W2 + static_cast<long long>(min(I0 + r, g.Nz - 1)) * g.P + J0);
-    w[r][0] = wv.x, w[r][1] = wv.y, w[r][2] = wv.z, w[r][3] = wv.w;
+    w[r][0] = lo2(wv), w[r][1] = hi2(wv);
   }
   bool row_ok[RZ];
 #pragma unroll
   for (int r = 0; r < RZ; ++r) row_ok[r] = !SP || I0 + r < g.Nz;
   Damp<SP> dmp;
   dmp.init(g, I0, J0);
-  const int tile_id = blockIdx.y * g.ntx + blockIdx.x;
+  const int tile_id = by * g.ntx + bx;
   const int rb = p.trec_beg[tile_id], re = p.trec_beg[tile_id + 1];
-  const float amp = p.src_amp[p.n];
   const long long data_stride = static_cast<long long>(g.nt) * g.nrec;
-  if (nf > 0) mbar_wait(qbar, 0);
 
-  Ring cons;
   auto release = [&]() {
     __syncthreads();  // every thread is done with this stage
     cons.advance();
-    if (tid == 0 && issued < nitems) {
+    if (tid == 0) {
       fence_proxy_async();
-      issue_next();
+      prod.issue(p);
     }
   };
   auto sample = [&](const float* st, float* out) {  // d[n][r] = field^n[rec_r] from the staged tile
@@ -319,81 +413,89 @@ __device__ __forceinline__ void fwd_body(const CUtensorMap* mh, const CUtensorMa
     if (row_ok[r]) st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
   };
 
-  float Lb[RZ][4];
-  for (int s = 0; s < p.S; ++s) {
-    // ---------------- background u of shot s: L u^n (kept for the Born sources), leader updates u
-    {
-      const float* st = stages + cons.stage * STAGE_FLOATS;
-      mbar_wait(&bars[cons.stage], cons.phase);
-      float C[RZ][4];
-      lap_points(st, tx, ty, Lb, C);
-      if (leader) {
-        float* dst = p.pool + (static_cast<long long>(s * p.nslot + p.bg_slot) * 2 + par_new) * g.plane;
-        const int sI = p.src_I[p.shot0 + s], sJ = p.src_J[p.shot0 + s];
-#pragma unroll
-        for (int r = 0; r < RZ; ++r) {
-          const float4 pv = ld4(st + TILE_FLOATS + so + r * TX);
-          float v[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) v[i] = dmp.upd(r, i, C[r][i], f4(pv, i), w[r][i] * Lb[r][i]);
-          if (I0 + r == sI && sJ >= J0 && sJ < J0 + 4) {  // point source dt^2 s[n] / h^2 (/(1 + c))
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if (J0 + i == sJ) v[i] += amp * dmp_ci(dmp, r, i);
-          }
-          if (SP && p.ring_out != nullptr) {  // BOUNDARY store: the ring of u^{n+1}
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int q = ring_index(g, I0 + r, J0 + i);
-              if (q >= 0) p.ring_out[s * p.ring_shot_stride + q] = v[i];
-            }
-          }
-          store_row(dst, r, v);
-        }
-        // imaging-factor store s^n = 2 dt^2 / (v h^2) * L~u^n on the interior (FULL store / replay segments)
-        const int jc = J0 - g.c0;
-        if (p.s_out != nullptr && jc >= 0 && jc < g.PI) {
-#pragma unroll
-          for (int r = 0; r < RZ; ++r) {
-            const int iz = I0 + r - g.W;
-            if (iz < 0 || iz >= g.nz) continue;
-            const float4 ic = ldg4(p.imgc + static_cast<long long>(iz) * g.PI + jc);
-            float o[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int ix = J0 + i - g.W;
-              o[i] = (!SP || (ix >= 0 && ix < g.nx)) ? f4(ic, i) * Lb[r][i] : 0.0f;
-            }
-            st4(p.s_out + s * p.s_shot_stride + static_cast<long long>(iz) * g.PI + jc,
-                make_float4(o[0], o[1], o[2], o[3]));
-          }
-        }
-        if (re > rb && p.d_bg) sample(st, p.d_bg + (p.dbg_shot0 + s) * data_stride);
-      }
-      release();
-    }
-    // ---------------- Born fields du_k of shot s: source q_k L u^n
-    float* born_base = p.pool + (static_cast<long long>(s * p.nslot + p.born_slot0 + fb) * 2 + par_new) * g.plane;
-    for (int t = 0; t < nf; ++t) {
-      const float* st = stages + cons.stage * STAGE_FLOATS;
-      mbar_wait(&bars[cons.stage], cons.phase);
-      float L[RZ][4], C[RZ][4];
-      lap_points(st, tx, ty, L, C);
-      float* dst = born_base + static_cast<long long>(t) * 2 * g.plane;
-      const float* qk = qs + t * PT_FLOATS + so;
+  // ---------------- background u of shot s: L u^n (kept for the Born sources), leader updates u
+  float2 Lb[RZ][2];
+  {
+    const float* st = stages + cons.stage * FSTAGE_FLOATS;
+    mbar_wait(&bars[cons.stage], cons.phase);
+    float2 C[RZ][2];
+    lap_points(st, tx, ty, Lb, C);
+    if (leader) {
+      float* dst = p.pool + (static_cast<long long>(s * p.nslot + p.bg_slot) * 2 + par_new) * g.plane;
+      const int sI = p.src_I[p.shot0 + s], sJ = p.src_J[p.shot0 + s];
+      const float amp = p.src_amp[p.n];
 #pragma unroll
       for (int r = 0; r < RZ; ++r) {
         const float4 pv = ld4(st + TILE_FLOATS + so + r * TX);
-        const float4 qv = ld4(qk + r * TX);
         float v[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          v[i] = dmp.upd(r, i, C[r][i], f4(pv, i), fmaf(f4(qv, i), Lb[r][i], w[r][i] * L[r][i]));
+        for (int h = 0; h < 2; ++h) {
+          const float2 u = dmp.upd(r, h, C[r][h], half2of(pv, h), mul2(w[r][h], Lb[r][h]));
+          v[2 * h] = u.x, v[2 * h + 1] = u.y;
+        }
+        if (I0 + r == sI && sJ >= J0 && sJ < J0 + 4) {  // point source dt^2 s[n] / h^2 (/(1 + c))
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (J0 + i == sJ) v[i] += amp * dmp_ci(dmp, r, i);
+        }
+        if (SP && p.ring_out != nullptr) {  // BOUNDARY store: the ring of u^{n+1}
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int q = ring_index(g, I0 + r, J0 + i);
+            if (q >= 0) p.ring_out[s * p.ring_shot_stride + q] = v[i];
+          }
+        }
         store_row(dst, r, v);
       }
-      if (re > rb && p.d_born) sample(st, p.d_born + (static_cast<long long>(s) * p.K + fb + t) * data_stride);
-      release();
+      // imaging-factor store s^n = 2 dt^2 / (v h^2) * L~u^n on the interior (FULL store / replay segments)
+      const int jc = J0 - g.c0;
+      if (p.s_out != nullptr && jc >= 0 && jc < g.PI) {
+#pragma unroll
+        for (int r = 0; r < RZ; ++r) {
+          const int iz = I0 + r - g.W;
+          if (iz < 0 || iz >= g.nz) continue;
+          const float4 ic = ldg4(p.imgc + static_cast<long long>(iz) * g.PI + jc);
+          const float2 o01 = mul2(lo2(ic), Lb[r][0]), o23 = mul2(hi2(ic), Lb[r][1]);
+          float o[4] = {o01.x, o01.y, o23.x, o23.y};
+          if (SP) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int ix = J0 + i - g.W;
+              if (ix < 0 || ix >= g.nx) o[i] = 0.0f;
+            }
+          }
+          st4(p.s_out + s * p.s_shot_stride + static_cast<long long>(iz) * g.PI + jc,
+              make_float4(o[0], o[1], o[2], o[3]));
+        }
+      }
+      if (re > rb && p.d_bg) sample(st, p.d_bg + (p.dbg_shot0 + s) * data_stride);
     }
+    release();
+  }
+  // ---------------- Born fields du_k of shot s: source q_k L u^n
+  float* born_base = p.pool + (static_cast<long long>(s * p.nslot + p.born_slot0 + fb) * 2 + par_new) * g.plane;
+  for (int t = 0; t < nf; ++t) {
+    const float* st = stages + cons.stage * FSTAGE_FLOATS;
+    mbar_wait(&bars[cons.stage], cons.phase);
+    float2 L[RZ][2], C[RZ][2];
+    lap_points(st, tx, ty, L, C);
+    float* dst = born_base + static_cast<long long>(t) * 2 * g.plane;
+    const float* qk = st + TILE_FLOATS + PT_FLOATS + so;
+#pragma unroll
+    for (int r = 0; r < RZ; ++r) {
+      const float4 pv = ld4(st + TILE_FLOATS + so + r * TX);
+      const float4 qv = ld4(qk + r * TX);
+      float v[4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float2 u = dmp.upd(r, h, C[r][h], half2of(pv, h),
+                                 fma2(half2of(qv, h), Lb[r][h], mul2(w[r][h], L[r][h])));
+        v[2 * h] = u.x, v[2 * h + 1] = u.y;
+      }
+      store_row(dst, r, v);
+    }
+    if (re > rb && p.d_born) sample(st, p.d_born + (static_cast<long long>(s) * p.K + fb + t) * data_stride);
+    release();
   }
 }
 
@@ -408,20 +510,36 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
                     const __grid_constant__ CUtensorMap mq, const FwdParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stages = reinterpret_cast<float*>(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES_BYTES);
-  float* qs = reinterpret_cast<float*>(smem_raw + STAGES_BYTES + BAR_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + FSTAGES_BYTES);
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     tma_prefetch_desc(&mh);
     tma_prefetch_desc(&mt);
     tma_prefetch_desc(&mq);
-    for (int i = 0; i < NSTAGE + 1; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < NSTAGE_F; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (tile_is_interior(p.g, blockIdx.x * TX, blockIdx.y * TZ))
-    fwd_body<false>(&mh, &mt, &mq, p, stages, qs, bars);
-  else
-    fwd_body<true>(&mh, &mt, &mq, p, stages, qs, bars);
+  const int ntl = p.g.ntx * p.g.ntz;
+  const int U = p.S * p.G * ntl;
+  const int nstep = gridDim.x;
+  FwdProducer prod;
+  prod.mh = &mh, prod.mt = &mt, prod.mq = &mq, prod.stages = stages, prod.bars = bars;
+  prod.u = blockIdx.x, prod.t = 0, prod.U = U, prod.nstep = nstep, prod.ntl = ntl;
+  prod.pol_first = policy_evict_first(), prod.pol_last = policy_evict_last();
+  prod.decode(p);
+  if (threadIdx.x == 0 && threadIdx.y == 0)
+    for (int i = 0; i < NSTAGE_F; ++i) prod.issue(p);
+  RingF cons;
+  for (int u = blockIdx.x; u < U; u += nstep) {
+    const int s = u / (p.G * ntl);
+    const int rem = u - s * p.G * ntl;
+    const int grp = rem / ntl, tile = rem - grp * ntl;
+    const int bx = tile % p.g.ntx, by = tile / p.g.ntx;
+    if (tile_is_interior(p.g, bx * TX, by * TZ))
+      fwd_unit<false>(p, stages, bars, s, grp, bx, by, cons, prod);
+    else
+      fwd_unit<true>(p, stages, bars, s, grp, bx, by, cons, prod);
+  }
 }
 
 // ------------------------------------------------------------------------------------------------ backward
@@ -429,11 +547,12 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
 struct BwdParams {
   Geo g;
   int nslot;
+  int nlev;               // planes per slot (2: parity; 4: level & 3, after/between two-step launches)
   float* pool;
   int j;                  // computes lambda^j from lambda^{j+1} (halo) and lambda^{j+2} (pointwise)
   int update;             // compute lambda^j (j >= 2; lambda^1 is never used)
   int imaging;            // accumulate s^j lambda^{j+1} (j <= nt-2)
-  int slot0, F;           // adjoint fields in slots slot0 .. slot0 + F - 1; BWD_FG per CTA (grid.z)
+  int slot0, F;           // adjoint fields in slots slot0 .. slot0 + F - 1; BWD_FG per group
   int S;                  // shots of the batch (every CTA loops over them)
   const float* W2;
   const float* s_lvl;     // s^j for batch shot 0
@@ -459,12 +578,12 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   const int nf = min(p.F, fb + BWD_FG) - fb;
   if (nf <= 0) return;
   const int nitems = p.S * nf;
-  const int par_in = (p.j + 1) & 1, par_out = p.j & 1;
+  const int par_in = (p.j + 1) & (p.nlev - 1), par_out = p.j & (p.nlev - 1);
   int ps = 0, pt = 0, issued = 0;
   Ring prod;
   auto issue_next = [&]() {
     float* st = stages + prod.stage * STAGE_FLOATS;
-    const int pl = (ps * p.nslot + p.slot0 + fb + pt) * 2;
+    const int pl = (ps * p.nslot + p.slot0 + fb + pt) * p.nlev;
     mbar_expect_tx(&bars[prod.stage], TILE_BYTES + (p.update ? PT_BYTES : 0));
     tma_load_3d(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_in);
     if (p.update) tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_out);
@@ -533,22 +652,32 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
       }
     }
     if (any_img && s + 1 < p.S) load_sj(s + 1, snext);
-    float* out_base = p.pool + (static_cast<long long>(s * p.nslot + p.slot0 + fb) * 2 + par_out) * g.plane;
+    float* out_base = p.pool + (static_cast<long long>(s * p.nslot + p.slot0 + fb) * p.nlev + par_out) * g.plane;
 #pragma unroll
     for (int t = 0; t < BWD_FG; ++t) {
       if (t >= nf) break;
       const float* st = stages + cons.stage * STAGE_FLOATS;
-      float* dst = out_base + static_cast<long long>(t) * 2 * g.plane;
+      float* dst = out_base + static_cast<long long>(t) * p.nlev * g.plane;
       mbar_wait(&bars[cons.stage], cons.phase);
       float L[RZ][4], C[RZ][4];
-      lap_points(st, tx, ty, L, C);
+      {
+        float2 L2[RZ][2], C2[RZ][2];
+        lap_points(st, tx, ty, L2, C2);
+#pragma unroll
+        for (int r = 0; r < RZ; ++r)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            L[r][2 * h] = L2[r][h].x, L[r][2 * h + 1] = L2[r][h].y;
+            C[r][2 * h] = C2[r][h].x, C[r][2 * h + 1] = C2[r][h].y;
+          }
+      }
       if (p.update) {
 #pragma unroll
         for (int r = 0; r < RZ; ++r) {
           const float4 pv = ld4(st + TILE_FLOATS + so + r * TX);
           float v[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) v[i] = dmp.upd(r, i, C[r][i], f4(pv, i), w[r][i] * L[r][i]);
+          for (int i = 0; i < 4; ++i) v[i] = dmp.upd1(r, i, C[r][i], f4(pv, i), w[r][i] * L[r][i]);
           if (SP) {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -682,8 +811,16 @@ __device__ __forceinline__ void rev_body(const CUtensorMap* mh, const CUtensorMa
   for (int s = 0; s < p.S; ++s) {
     const float* st = stages + cons.stage * STAGE_FLOATS;
     mbar_wait(&bars[cons.stage], cons.phase);
+    float2 L2[RZ][2], C2[RZ][2];
+    lap_points(st, tx, ty, L2, C2);
     float L[RZ][4], C[RZ][4];
-    lap_points(st, tx, ty, L, C);
+#pragma unroll
+    for (int r = 0; r < RZ; ++r)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        L[r][2 * h] = L2[r][h].x, L[r][2 * h + 1] = L2[r][h].y;
+        C[r][2 * h] = C2[r][h].x, C[r][2 * h + 1] = C2[r][h].y;
+      }
     float* dst = p.pool + (static_cast<long long>(s * p.nslot + p.slot) * 2 + par_o) * g.plane;
     const int sI = p.src_I[p.shot0 + s], sJ = p.src_J[p.shot0 + s];
 #pragma unroll
@@ -804,7 +941,9 @@ __global__ void q_setup_kernel(Geo g, const float* __restrict__ m, const float* 
 }
 
 // d[n = nt-1] for every field of the batch: the level the last forward step produced.
-__global__ void gather_last_kernel(Geo g, const float* __restrict__ pool, int nslot, int par, int dbg_shot0,
+// Pool planes per slot: nlev (2: parity planes of the single-step kernels; 4: level & 3 of fwd2); par = the
+// plane of level nt-1 within a slot.
+__global__ void gather_last_kernel(Geo g, const float* __restrict__ pool, int nslot, int nlev, int par, int dbg_shot0,
                                     float* d_bg, int bg_slot, float* d_born, int born_slot0, int K,
                                     const int* rec_I, const int* rec_J) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -814,11 +953,11 @@ __global__ void gather_last_kernel(Geo g, const float* __restrict__ pool, int ns
   const long long off = static_cast<long long>(rec_I[r]) * g.P + rec_J[r];
   if (f == 0) {
     if (!d_bg) return;
-    const long long pl = (static_cast<long long>(s) * nslot + bg_slot) * 2 + par;
+    const long long pl = (static_cast<long long>(s) * nslot + bg_slot) * nlev + par;
     d_bg[(static_cast<long long>(dbg_shot0 + s) * g.nt + (g.nt - 1)) * g.nrec + r] = pool[pl * g.plane + off];
   } else {
     if (!d_born) return;
-    const long long pl = (static_cast<long long>(s) * nslot + born_slot0 + f - 1) * 2 + par;
+    const long long pl = (static_cast<long long>(s) * nslot + born_slot0 + f - 1) * nlev + par;
     d_born[((static_cast<long long>(s) * K + (f - 1)) * g.nt + (g.nt - 1)) * g.nrec + r] =
         pool[pl * g.plane + off];
   }

@@ -76,7 +76,7 @@ typedef struct {
   int32_t store;         /* HV_STORE_* (AUTO: FULL if it fits, else CHECKPOINT)                         */
   int32_t ckpt_interval; /* CHECKPOINT spacing in levels; 0 = round(sqrt(nt))                            */
   int32_t shot_batch;    /* shots propagated concurrently; 0 = auto from the memory budget               */
-  int32_t field_group;   /* max Born fields per forward work unit (tuning); 0 = auto (11)                 */
+  int32_t field_group;   /* max Born fields per forward work unit (tuning); 0 = auto (16)                 */
   int32_t device;        /* CUDA device ordinal                                                          */
   size_t  mem_budget;    /* bytes of device memory the plan may use; 0 = 90 % of free memory             */
 } hv_config;

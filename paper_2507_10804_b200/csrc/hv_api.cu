@@ -119,7 +119,7 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
   const int ntiles = g.ntx * g.ntz;
   // forward Born fields per unit (max; groups are near-equal): fewer groups = fewer background recomputes per
   // shot and tile, more groups = finer load balance over the one-wave grid
-  pl->FG = std::min(FWD_FG_MAX, c->cfg.field_group > 0 ? c->cfg.field_group : 11);
+  pl->FG = std::min(FWD_FG_MAX, c->cfg.field_group > 0 ? c->cfg.field_group : 16);
   (void)ntiles;
   if (S <= 0) S = 32;  // every CTA loops over the batch's shots: more shots amortise q_k loads and imaging writes
   S = std::min(S, fit);

@@ -41,6 +41,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -96,6 +99,24 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
+}
+// Global accesses with an L2 eviction-priority policy (the streaming side of the same scheme).
+__device__ __forceinline__ float4 ldg4_hint(const float* p, uint64_t policy) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(policy));
+  return v;
+}
+__device__ __forceinline__ void st4_hint(float* p, float4 v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void red4_hint(float* p, float4 v, uint64_t policy) {
+  asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(policy)
+               : "memory");
 }
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -299,6 +320,21 @@ using RingF = RingN<NSTAGE_F>;  // forward kernel
 #ifndef HV_L2_HINTS
 #define HV_L2_HINTS 1
 #endif
+#ifndef HV_FWD_EMPTY
+#define HV_FWD_EMPTY 1  // forward: per-stage empty mbarriers instead of a block barrier per item
+#endif
+#ifndef HV_BWD_EMPTY
+#define HV_BWD_EMPTY 0  // backward: per-stage empty mbarriers (block barrier only on tiles with receivers); slower
+#endif
+#ifndef HV_UNIT_ORDER_GST
+#define HV_UNIT_ORDER_GST 1  // forward units in (group, shot, tile) order: a group's q_k tiles stay L2-resident
+#endif
+#ifndef HV_ST_HINT
+#define HV_ST_HINT 0  // field stores evict_first
+#endif
+#ifndef HV_BWD_HINTS
+#define HV_BWD_HINTS 0  // adjoint: lambda^{j+2} tiles and s^j loads evict_first, imaging RED evict_last
+#endif
 // Born fields of forward group grp: [group_begin(grp), group_begin(grp + 1)), G near-equal groups.
 __device__ __forceinline__ int group_begin(int K, int G, int grp) { return (K * grp) / G; }
 
@@ -312,11 +348,27 @@ struct FwdProducer {  // thread 0's walk over this CTA's items (decoded once per
   bool upd;
   uint64_t pol_first, pol_last;
   RingF ring;
+  RingF ering;       // stage whose consumers the next refill waits for
+  int consumed = 0;  // items this CTA's warp 0 has finished
+  // Barrier-free refill (HV_FWD_EMPTY): after warp 0 finishes item c - 1, refill the stage of item c - 2 once
+  // all consumer warps have released it (empty barrier), i.e. one item of slack for the slowest warp.
+  __device__ __forceinline__ void after_consume(const FwdParams& p, uint64_t* empty) {
+    if (++consumed < 2) return;
+    mbar_wait(&empty[ering.stage], ering.phase);
+    ering.advance();
+    issue(p);
+  }
   __device__ __forceinline__ void decode(const FwdParams& p) {
     if (u >= U) return;
+#if HV_UNIT_ORDER_GST
+    const int grp = u / (p.S * ntl);
+    const int rem = u - grp * p.S * ntl;
+    const int s = rem / ntl, tile = rem - s * ntl;
+#else
     const int s = u / (p.G * ntl);
     const int rem = u - s * p.G * ntl;
     const int grp = rem / ntl, tile = rem - grp * ntl;
+#endif
     const int by = tile / p.g.ntx;
     x0 = (tile - by * p.g.ntx) * TX, z0 = by * TZ;
     fb = group_begin(p.K, p.G, grp);
@@ -390,12 +442,19 @@ __device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages
   const long long data_stride = static_cast<long long>(g.nt) * g.nrec;
 
   auto release = [&]() {
+#if HV_FWD_EMPTY
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&bars[NSTAGE_F + cons.stage]);  // this warp is done with the stage
+    cons.advance();
+    if (tid == 0) prod.after_consume(p, bars + NSTAGE_F);
+#else
     __syncthreads();  // every thread is done with this stage
     cons.advance();
     if (tid == 0) {
       fence_proxy_async();
       prod.issue(p);
     }
+#endif
   };
   auto sample = [&](const float* st, float* out) {  // d[n][r] = field^n[rec_r] from the staged tile
     for (int q = rb + tid; q < re; q += NTHREADS) {
@@ -410,7 +469,12 @@ __device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages
       for (int i = 0; i < 4; ++i)
         if (J0 + i >= g.Nx) v[i] = 0.0f;
     }
+#if HV_ST_HINT
+    if (row_ok[r])
+      st4_hint(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]), prod.pol_first);
+#else
     if (row_ok[r]) st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
+#endif
   };
 
   // ---------------- background u of shot s: L u^n (kept for the Born sources), leader updates u
@@ -516,6 +580,7 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
     tma_prefetch_desc(&mt);
     tma_prefetch_desc(&mq);
     for (int i = 0; i < NSTAGE_F; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < NSTAGE_F; ++i) mbar_init(&bars[NSTAGE_F + i], NTHREADS / 32);  // empty: one per warp
     fence_mbar_init();
   }
   __syncthreads();
@@ -531,9 +596,15 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
     for (int i = 0; i < NSTAGE_F; ++i) prod.issue(p);
   RingF cons;
   for (int u = blockIdx.x; u < U; u += nstep) {
+#if HV_UNIT_ORDER_GST
+    const int grp = u / (p.S * ntl);
+    const int rem = u - grp * p.S * ntl;
+    const int s = rem / ntl, tile = rem - s * ntl;
+#else
     const int s = u / (p.G * ntl);
     const int rem = u - s * p.G * ntl;
     const int grp = rem / ntl, tile = rem - grp * ntl;
+#endif
     const int bx = tile % p.g.ntx, by = tile / p.g.ntx;
     if (tile_is_interior(p.g, bx * TX, by * TZ))
       fwd_unit<false>(p, stages, bars, s, grp, bx, by, cons, prod);
@@ -579,6 +650,8 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   if (nf <= 0) return;
   const int nitems = p.S * nf;
   const int par_in = (p.j + 1) & (p.nlev - 1), par_out = p.j & (p.nlev - 1);
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+  (void)pol_last;
   int ps = 0, pt = 0, issued = 0;
   Ring prod;
   auto issue_next = [&]() {
@@ -586,7 +659,11 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
     const int pl = (ps * p.nslot + p.slot0 + fb + pt) * p.nlev;
     mbar_expect_tx(&bars[prod.stage], TILE_BYTES + (p.update ? PT_BYTES : 0));
     tma_load_3d(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_in);
+#if HV_BWD_HINTS
+    if (p.update) tma_load_3d_hint(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_out, pol_first);
+#else
     if (p.update) tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_out);
+#endif
     prod.advance();
     if (++pt == nf) {
       pt = 0;
@@ -621,8 +698,14 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
 #pragma unroll
     for (int r = 0; r < RZ; ++r) {
       dst[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+#if HV_BWD_HINTS
+      if (img_rows[r])
+        dst[r] = ldg4_hint(p.s_lvl + s * p.s_shot_stride + static_cast<long long>(I0 + r - g.W) * g.PI + jc,
+                           pol_first);
+#else
       if (img_rows[r])
         dst[r] = ldg4(p.s_lvl + s * p.s_shot_stride + static_cast<long long>(I0 + r - g.W) * g.PI + jc);
+#endif
     }
   };
   float4 snext[RZ];
@@ -641,6 +724,9 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
       for (int i = 0; i < 4; ++i) acc[t][r][i] = 0.0f;
 
   Ring cons;
+  Ring erel;          // HV_BWD_EMPTY: stage the next refill waits on
+  int consumed = 0;
+  (void)erel, (void)consumed;
   for (int s = 0; s < p.S; ++s) {
     float sj[RZ][4];
 #pragma unroll
@@ -683,7 +769,12 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
             for (int i = 0; i < 4; ++i)
               if (J0 + i >= g.Nx) v[i] = 0.0f;
           }
+#if HV_ST_HINT
+          if (row_ok[r])
+            st4_hint(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]), pol_first);
+#else
           if (row_ok[r]) st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
+#endif
         }
       }
       // zero-lag imaging, summed over the batch's shots in registers: acc += s^j * lambda^{j+1}
@@ -691,12 +782,27 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
       for (int r = 0; r < RZ; ++r)
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[t][r][i] = fmaf(sj[r][i], C[r][i], acc[t][r][i]);
+#if HV_BWD_EMPTY
+      // release the stage per warp (empty barrier); warp 0 refills the stage of the item before this one once
+      // every warp has released it. Only tiles with receivers need a block barrier: the injection below adds
+      // into points other warps store.
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&bars[NSTAGE + cons.stage]);
+      cons.advance();
+      if (tid == 0 && ++consumed >= 2) {
+        mbar_wait(&bars[NSTAGE + erel.stage], erel.phase);
+        erel.advance();
+        if (issued < nitems) issue_next();
+      }
+      if (p.update && re > rb) __syncthreads();  // lambda^j of this tile stored (uniform per CTA)
+#else
       __syncthreads();  // stage consumed and lambda^j of this tile stored
       cons.advance();
       if (tid == 0 && issued < nitems) {
         fence_proxy_async();
         issue_next();
       }
+#endif
       // receiver injection into lambda^j: += v^2 / (1 + c) * rho[j][r]   (R^T scatter-add)
       if (p.update && re > rb) {
         const int slot = p.slot0 + fb + t;
@@ -718,8 +824,13 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
 #pragma unroll
       for (int r = 0; r < RZ; ++r) {
         if (!img_rows[r]) continue;
+#if HV_BWD_HINTS
+        red4_hint(a + static_cast<long long>(r) * g.P,
+                  make_float4(acc[t][r][0], acc[t][r][1], acc[t][r][2], acc[t][r][3]), pol_last);
+#else
         atomicAdd(reinterpret_cast<float4*>(a + static_cast<long long>(r) * g.P),
                   make_float4(acc[t][r][0], acc[t][r][1], acc[t][r][2], acc[t][r][3]));
+#endif
       }
     }
   }
@@ -735,6 +846,7 @@ __global__ void __launch_bounds__(NTHREADS, HV_BWD_MINB)
     tma_prefetch_desc(&mh);
     tma_prefetch_desc(&mt);
     for (int i = 0; i < NSTAGE; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < NSTAGE; ++i) mbar_init(&bars[NSTAGE + i], NTHREADS / 32);
     fence_mbar_init();
   }
   __syncthreads();

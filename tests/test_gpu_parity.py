@@ -170,6 +170,29 @@ def test_deterministic_and_batch_invariant(hv, ragged):
     assert np.array_equal(c[0], a[1])
 
 
+@pytest.mark.parametrize("nt", [300, 301])
+def test_two_step_kernels_bitwise_equal_single_step(hv, ragged, nt, monkeypatch):
+    """The two-step kernels (fwd2 / bwd2, FULL store) compute every field level with the single-step kernels'
+    exact per-point operations: d is bitwise identical with HV_T2=0 (single-step). The imaging sums add the two
+    levels of a launch per shot before the shot sum (the single-step kernel adds one level per launch), so g, phi
+    and H·v agree to fp32 summation-order rounding. Even and odd numbers of steps (nt - 1): with and without a
+    trailing single-level launch."""
+    wl, V, d, HV, d_obs, phi, g, m_start = ragged
+    wl = W.custom(70, 150, nt=nt, ns=3, nrec=37, n_probes=3, f_peak=15.0, seed=5)
+    d_obs = d_obs[:, :nt] if nt <= d_obs.shape[1] else np.pad(d_obs, ((0, 0), (0, nt - d_obs.shape[1]), (0, 0)))
+    out = {}
+    for t2 in ("1", "0"):
+        monkeypatch.setenv("HV_T2", t2)
+        s = hv.Solver.from_workload(wl, store="full", shot_batch=2, field_group=2)
+        out[t2] = (s.forward(wl.model), s.gradient(m_start, d_obs), s.hessvec(wl.model, V))
+    (d1, (p1, g1), h1), (d0, (p0, g0), h0) = out["1"], out["0"]
+    assert np.array_equal(d1, d0)
+    assert abs(p1 - p0) <= 1e-12 * abs(p0)           # phi depends on d only (fp64 block sums, atomic order)
+    assert rel_l2(g1, g0) <= 1e-6 and rel_l2(h1, h0) <= 1e-6
+    if nt == 300:
+        assert rel_l2(h1, HV) <= TOL
+
+
 def test_edge_cases(hv):
     # degenerate: zero probe -> zero H v, zero residual -> zero gradient; minimum grid; receiver on a corner
     wl = W.custom(1, 5, nt=40, ns=1, nrec=2, n_probes=1, W=4, f_peak=25.0, seed=2)

@@ -48,6 +48,14 @@ int make_tmap(hv_ctx* c, const float* base, long long nplanes, int box_w, int bo
 }
 
 constexpr bool kTwoStepDefault = false;
+// Backward CTAs per (tile, field group): the batch's shots are split into this many parts, each summing its
+// imaging terms into its own accumulator copy (finalize adds the copies in a fixed order). 2 halves the last
+// partial wave of the backward grid at the cost of one more RED per point and field per launch; measured on
+// cfg 1: 1 -> 273.9 us, 2 -> 273.8 us, 4 -> 287 us per launch, so the default keeps one part.
+#ifndef HV_BWD_SPLIT
+#define HV_BWD_SPLIT 1
+#endif
+constexpr int kBwdSplit = HV_BWD_SPLIT;
 
 int grid1d(long long n) { return static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16)); }
 
@@ -82,7 +90,7 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
   double budget = c->cfg.mem_budget ? static_cast<double>(c->cfg.mem_budget) : 0.9 * static_cast<double>(freeb);
   // shared (not per shot): Q, W2, imgc, rec coef, staging of V/HV/m
   const double shared = F4 * (static_cast<double>(K) * g.plane * 2 + g.plane + g.iplane + 4.0 * K * g.nz * g.nx +
-                              2.0 * g.nz * g.nx + (double)pl->nacc * g.plane) + (1 << 20);
+                              2.0 * g.nz * g.nx + (double)kBwdSplit * pl->nacc * g.plane) + (1 << 20);
   auto per_shot = [&](int store, int k) {
     double b = F4 * (store == HV_STORE_FULL ? 4.0 : 2.0) * pl->nslot * g.plane;  // field pool
     b += F4 * (double)K * g.nt * g.nrec;                                        // Born data
@@ -217,8 +225,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     if ((st = ws_get(c, "rres", sizeof(float) * (size_t)S * g.nt * g.nrec, (void**)&rres))) return st;
   }
   if (adjoint) {
-    if ((st = ws_get(c, "acc", sizeof(float) * g.plane * pl.nacc, (void**)&acc))) return st;
-    CU_TRY(cudaMemsetAsync(acc, 0, sizeof(float) * g.plane * pl.nacc, c->stream));
+    if ((st = ws_get(c, "acc", sizeof(float) * g.plane * pl.nacc * kBwdSplit, (void**)&acc))) return st;
+    CU_TRY(cudaMemsetAsync(acc, 0, sizeof(float) * g.plane * pl.nacc * kBwdSplit, c->stream));
     if (pl.store == HV_STORE_FULL) {
       if ((st = ws_get(c, "store", sizeof(float) * g.iplane * g.nt * S, (void**)&store))) return st;
     } else if (pl.store == HV_STORE_BOUNDARY) {
@@ -402,6 +410,9 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
       bp.pool = pool;
       bp.nslot = nslot;
       bp.nlev = pl.nlev;
+      bp.G = Gb;
+      bp.nsplit = std::min(kBwdSplit, Sb);
+      bp.acc_copy = static_cast<long long>(pl.nacc) * g.plane;
       bp.slot0 = slot0_b;
       bp.F = Fb;
       bp.S = Sb;
@@ -415,7 +426,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
       bp.trec_id = c->d_trec_id;
       bp.rec_I = c->d_recI;
       bp.rec_J = c->d_recJ;
-      const dim3 gridb(g.ntx, g.ntz, Gb);
+      const dim3 gridb(g.ntx, g.ntz, Gb * bp.nsplit);
       if (e_b0) CU_TRY(cudaEventRecord(e_b0, c->stream));
       int cur_b = -1;
       int j_t1 = g.nt - 1;  // first level left for the single-step kernel
@@ -578,13 +589,13 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
 
   // --- a8 (within the GPU): fixed-order sum over the shots in flight, into the caller's layout
   if (grad) {
-    finalize_kernel<<<grid1d((long long)g.nz * g.nx), 256, 0, c->stream>>>(g, acc, 1, pl.nacc, 0, 1,
+    finalize_kernel<<<grid1d((long long)g.nz * g.nx), 256, 0, c->stream>>>(g, acc, kBwdSplit, pl.nacc, 0, 1,
                                                                              reinterpret_cast<float*>(o_g.dev));
     launches++;
   }
   if (K > 0) {
     finalize_kernel<<<grid1d((long long)K * g.nz * g.nx), 256, 0, c->stream>>>(
-        g, acc, 1, pl.nacc, 1, K, reinterpret_cast<float*>(o_hv.dev));
+        g, acc, kBwdSplit, pl.nacc, 1, K, reinterpret_cast<float*>(o_hv.dev));
     launches++;
   }
   CU_TRY(cudaGetLastError());

@@ -624,7 +624,10 @@ struct BwdParams {
   int update;             // compute lambda^j (j >= 2; lambda^1 is never used)
   int imaging;            // accumulate s^j lambda^{j+1} (j <= nt-2)
   int slot0, F;           // adjoint fields in slots slot0 .. slot0 + F - 1; BWD_FG per group
-  int S;                  // shots of the batch (every CTA loops over them)
+  int S;                  // shots of the batch
+  int G;                  // field groups (grid.z = nsplit x G)
+  int nsplit;             // shot parts: part h loops over shots [h S / nsplit, (h+1) S / nsplit)
+  long long acc_copy;     // floats between the per-part accumulator copies (single writer per copy and launch)
   const float* W2;
   const float* s_lvl;     // s^j for batch shot 0
   long long s_shot_stride;
@@ -645,14 +648,17 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   const Geo& g = p.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
   const int x0 = blockIdx.x * TX, z0 = blockIdx.y * TZ;
-  const int fb = blockIdx.z * BWD_FG;
+  // grid.z = (shot part h) x (field group): part h owns the batch's shots [sb, se) and its own accumulator copy
+  const int h = blockIdx.z / p.G, grp = blockIdx.z - h * p.G;
+  const int sb = (h * p.S) / p.nsplit, se = ((h + 1) * p.S) / p.nsplit;
+  const int fb = grp * BWD_FG;
   const int nf = min(p.F, fb + BWD_FG) - fb;
-  if (nf <= 0) return;
-  const int nitems = p.S * nf;
+  if (nf <= 0 || se <= sb) return;
+  const int nitems = (se - sb) * nf;
   const int par_in = (p.j + 1) & (p.nlev - 1), par_out = p.j & (p.nlev - 1);
   const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
   (void)pol_last;
-  int ps = 0, pt = 0, issued = 0;
+  int ps = sb, pt = 0, issued = 0;
   Ring prod;
   auto issue_next = [&]() {
     float* st = stages + prod.stage * STAGE_FLOATS;
@@ -709,7 +715,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
     }
   };
   float4 snext[RZ];
-  load_sj(0, snext);
+  load_sj(sb, snext);
   BwdDamp<SP> dmp;
   dmp.init(g, I0, J0);
   const int tile_id = blockIdx.y * g.ntx + blockIdx.x;
@@ -727,7 +733,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   Ring erel;          // HV_BWD_EMPTY: stage the next refill waits on
   int consumed = 0;
   (void)erel, (void)consumed;
-  for (int s = 0; s < p.S; ++s) {
+  for (int s = sb; s < se; ++s) {
     float sj[RZ][4];
 #pragma unroll
     for (int r = 0; r < RZ; ++r) {
@@ -737,7 +743,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
         sj[r][i] = (!SP || (ix >= 0 && ix < g.nx)) ? f4(snext[r], i) : 0.0f;
       }
     }
-    if (any_img && s + 1 < p.S) load_sj(s + 1, snext);
+    if (any_img && s + 1 < se) load_sj(s + 1, snext);
     float* out_base = p.pool + (static_cast<long long>(s * p.nslot + p.slot0 + fb) * p.nlev + par_out) * g.plane;
 #pragma unroll
     for (int t = 0; t < BWD_FG; ++t) {
@@ -820,7 +826,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
 #pragma unroll
     for (int t = 0; t < BWD_FG; ++t) {
       if (t >= nf) break;
-      float* a = p.acc + static_cast<long long>(p.slot0 + fb + t) * g.plane + go;
+      float* a = p.acc + h * p.acc_copy + static_cast<long long>(p.slot0 + fb + t) * g.plane + go;
 #pragma unroll
       for (int r = 0; r < RZ; ++r) {
         if (!img_rows[r]) continue;

@@ -188,6 +188,9 @@ def main():
     ap.add_argument("--ref-nt", type=int, default=300)
     ap.add_argument("--cpu-nt", type=int, default=1000)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shots", type=int, default=0,
+                    help="evidence runs only: first N shots of the config (the JSON config says so)")
+    ap.add_argument("--nt", type=int, default=0, help="evidence runs only: truncated time axis")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -207,6 +210,8 @@ def main():
     from paper_2507_10804_b200.dist import shard_range
 
     wl = W.config(args.config)
+    if args.shots or args.nt:  # reduced evidence run (never the driver's bench line)
+        wl = wl.subset(shots=range(args.shots) if args.shots else None, nt=args.nt or None)
     K = wl.n_probes
     ns = wl.ns
     b, e = shard_range(ns, ws, rank)
@@ -321,7 +326,9 @@ def main():
             "metric": "hessian_vector_products_per_s", "value": value, "unit": "H·v/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"cfg{args.config}", "model": "quadratic-depth v(z)" if args.config == 1
+            "config": {"workload": f"cfg{args.config}" + (f" (first {wl.ns} shots, nt {wl.nt}: evidence run)"
+                                                          if args.shots or args.nt else ""),
+                       "model": "quadratic-depth v(z)" if args.config == 1
                        else wl.name, "grid": [wl.nz, wl.nx], "shots": ns, "probes": K, "nt": wl.nt,
                        "global_batch": K, "parallelism": f"dp{ws} (source-sharded, NCCL all-reduce of H·v)",
                        "l2": "flushed (256 MiB write) between timed steps",

@@ -87,12 +87,25 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
     cudaGetLastError();
     return fail(c, HV_ECUDA, "cudaMemGetInfo failed");
   }
-  double budget = c->cfg.mem_budget ? static_cast<double>(c->cfg.mem_budget) : 0.9 * static_cast<double>(freeb);
+  // the context's own workspace (grow-only, reused or re-allocated by this call) counts as available
+  // (only the buffers of the H·v path: callers such as hv_lowrank_geneig hold their own across hv_hessvec calls)
+  static const char* const kPathBufs[] = {"W2",   "imgc", "rec_coef", "scalars", "Q",    "pool", "dborn", "dbg",
+                                          "rres", "acc",  "store",    "ring",    "sbuf", "ckpt", "seg"};
+  double held = 0;
+  for (const char* n : kPathBufs) {
+    auto it = c->ws.find(n);
+    if (it != c->ws.end()) held += static_cast<double>(it->second.bytes);
+  }
+  double budget = c->cfg.mem_budget ? static_cast<double>(c->cfg.mem_budget)
+                                    : 0.9 * (static_cast<double>(freeb) + held);
+  // two-step kernels (fwd2 / bwd2) for FULL-store and forward-only calls; HV_T2=0 forces the single-step ones
+  const char* t2 = std::getenv("HV_T2");
+  const bool t2_on = t2 ? std::strcmp(t2, "0") != 0 : kTwoStepDefault;
   // shared (not per shot): Q, W2, imgc, rec coef, staging of V/HV/m
   const double shared = F4 * (static_cast<double>(K) * g.plane * 2 + g.plane + g.iplane + 4.0 * K * g.nz * g.nx +
                               2.0 * g.nz * g.nx + (double)kBwdSplit * pl->nacc * g.plane) + (1 << 20);
   auto per_shot = [&](int store, int k) {
-    double b = F4 * (store == HV_STORE_FULL ? 4.0 : 2.0) * pl->nslot * g.plane;  // field pool
+    double b = F4 * (store == HV_STORE_FULL && t2_on ? 4.0 : 2.0) * pl->nslot * g.plane;  // field pool
     b += F4 * (double)K * g.nt * g.nrec;                                        // Born data
     if (grad) b += F4 * 2.0 * g.nt * g.nrec;                                    // data + residual
     if (adjoint) {
@@ -111,9 +124,6 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
   if (store != HV_STORE_FULL && store != HV_STORE_CHECKPOINT && store != HV_STORE_BOUNDARY)
     return fail(c, HV_EINVAL, "unknown storage mode " + std::to_string(store));
   pl->store = store;
-  // two-step kernels (fwd2 / bwd2) for FULL-store and forward-only calls; HV_T2=0 forces the single-step ones
-  const char* t2 = std::getenv("HV_T2");
-  const bool t2_on = t2 ? std::strcmp(t2, "0") != 0 : kTwoStepDefault;
   pl->nlev = (store == HV_STORE_FULL && t2_on) ? 4 : 2;
   pl->k = k;
   pl->nck = (g.nt - 1 + k - 1) / k;
@@ -131,8 +141,24 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
   (void)ntiles;
   if (S <= 0) S = 32;  // every CTA loops over the batch's shots: more shots amortise q_k loads and imaging writes
   S = std::min(S, fit);
-  S = std::min(S, c->nloc);
-  pl->S = std::max(1, S);
+  S = std::max(1, std::min(S, c->nloc));
+  if (c->cfg.shot_batch <= 0) {  // equal batches: ceil(nloc / S) batches of near-equal size (no 1-shot tail)
+    const int nb = (c->nloc + S - 1) / S;
+    S = (c->nloc + nb - 1) / nb;
+  }
+  pl->S = S;
+  // a plan that needs the memory the workspace holds releases it first (buffers are re-allocated at their new
+  // sizes by this call; captured graphs refer to the old addresses and are dropped with them)
+  if (!c->cfg.mem_budget && shared + pl->S * pl->per_shot > 0.9 * static_cast<double>(freeb) && held > 0) {
+    for (auto& kv : c->graphs) kv.second.destroy();
+    c->graphs.clear();
+    for (const char* n : kPathBufs) {
+      auto it = c->ws.find(n);
+      if (it == c->ws.end()) continue;
+      if (it->second.p) cudaFree(it->second.p);
+      c->ws.erase(it);
+    }
+  }
   return HV_OK;
 }
 
@@ -485,7 +511,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
             rv.src_I = c->d_srcI;
             rv.src_J = c->d_srcJ;
             rv.src_amp = c->d_src_amp;
-            rev_step_kernel<<<dim3(g.ntx, g.ntz, 1), block, BWD_SMEM_BYTES, c->stream>>>(map_halo, map_tile, rv);
+            rev_step_kernel<<<dim3(g.ntx, g.ntz, Sb), block, BWD_SMEM_BYTES, c->stream>>>(map_halo, map_tile, rv);
             launches++;
             bp.s_lvl = rv.s_out;
             bp.s_shot_stride = g.iplane;

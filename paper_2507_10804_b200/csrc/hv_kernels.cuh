@@ -55,21 +55,39 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the warp is parked (not spinning on issue slots) until the phase completes
+// or the hint (ns) expires.
+#ifndef HV_WAIT_HINT_NS
+#define HV_WAIT_HINT_NS 1000000
+#endif
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(HV_WAIT_HINT_NS)
+      : "memory");
+  return ok != 0;
+}
 // Waits for the phase; a pipeline bug that would hang the GPU traps instead after ~2^34 cycles (~9 s), so the
-// call fails with a CUDA error rather than wedging the device.
+// call fails with a CUDA error rather than wedging the device. The clock is read once per 64 failed polls so
+// the guard costs no issue slots in the common case.
 #ifndef HV_WAIT_GUARD
 #define HV_WAIT_GUARD 1
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #if !HV_WAIT_GUARD
-  while (!mbar_try_wait(bar, parity)) {
+  while (!mbar_try_wait_hint(bar, parity)) {
   }
   return;
 #endif
-  if (mbar_try_wait(bar, parity)) return;
+  if (mbar_try_wait_hint(bar, parity)) return;
   const long long t0 = clock64();
-  while (!mbar_try_wait(bar, parity)) {
-    if (clock64() - t0 > (1LL << 34)) __trap();
+  for (uint32_t k = 1;; ++k) {
+    if (mbar_try_wait_hint(bar, parity)) return;
+    if ((k & 63u) == 0 && clock64() - t0 > (1LL << 34)) __trap();
   }
 }
 __device__ __forceinline__ void tma_load_3d(float* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
@@ -99,24 +117,6 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
-}
-// Global accesses with an L2 eviction-priority policy (the streaming side of the same scheme).
-__device__ __forceinline__ float4 ldg4_hint(const float* p, uint64_t policy) {
-  float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p), "l"(policy));
-  return v;
-}
-__device__ __forceinline__ void st4_hint(float* p, float4 v, uint64_t policy) {
-  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y),
-               "f"(v.z), "f"(v.w), "l"(policy)
-               : "memory");
-}
-__device__ __forceinline__ void red4_hint(float* p, float4 v, uint64_t policy) {
-  asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
-               "f"(v.y), "f"(v.z), "f"(v.w), "l"(policy)
-               : "memory");
 }
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -178,11 +178,17 @@ __device__ __forceinline__ void lap_points_w(const float* __restrict__ t, int tx
       const int i = 2 * h;
       auto P = [&](int k) { return make_float2(xs[k + i], xs[k + i + 1]); };
       auto Z = [&](int k) { return half2of(zw[r + k], h); };
+      // x-pair sum at distance d: even d reads register-aligned pairs (one FADD2); odd d straddles the float4s,
+      // so two scalar FADDs (same roundings) write the aligned result pair instead of MOV-ing operands together
+      auto X = [&](int d) {
+        if (d % 2 == 0) return add2(P(4 - d), P(4 + d));
+        return make_float2(__fadd_rn(xs[4 - d + i], xs[4 + d + i]), __fadd_rn(xs[5 - d + i], xs[5 + d + i]));
+      };
       const float2 ctr = P(4);
-      float2 s = mul2(splat2(HV_A1), add2(add2(P(3), P(5)), add2(Z(3), Z(5))));
-      s = fma2(splat2(HV_A2), add2(add2(P(2), P(6)), add2(Z(2), Z(6))), s);
-      s = fma2(splat2(HV_A3), add2(add2(P(1), P(7)), add2(Z(1), Z(7))), s);
-      s = fma2(splat2(HV_A4), add2(add2(P(0), P(8)), add2(Z(0), Z(8))), s);
+      float2 s = mul2(splat2(HV_A1), add2(X(1), add2(Z(3), Z(5))));
+      s = fma2(splat2(HV_A2), add2(X(2), add2(Z(2), Z(6))), s);
+      s = fma2(splat2(HV_A3), add2(X(3), add2(Z(1), Z(7))), s);
+      s = fma2(splat2(HV_A4), add2(X(4), add2(Z(0), Z(8))), s);
       L[r][h] = fma2(splat2(2.0f * HV_A0), ctr, s);
       C[r][h] = ctr;
     }
@@ -323,18 +329,6 @@ using RingF = RingN<NSTAGE_F>;  // forward kernel
 #ifndef HV_FWD_EMPTY
 #define HV_FWD_EMPTY 1  // forward: per-stage empty mbarriers instead of a block barrier per item
 #endif
-#ifndef HV_BWD_EMPTY
-#define HV_BWD_EMPTY 0  // backward: per-stage empty mbarriers (block barrier only on tiles with receivers); slower
-#endif
-#ifndef HV_UNIT_ORDER_GST
-#define HV_UNIT_ORDER_GST 1  // forward units in (group, shot, tile) order: a group's q_k tiles stay L2-resident
-#endif
-#ifndef HV_ST_HINT
-#define HV_ST_HINT 0  // field stores evict_first
-#endif
-#ifndef HV_BWD_HINTS
-#define HV_BWD_HINTS 0  // adjoint: lambda^{j+2} tiles and s^j loads evict_first, imaging RED evict_last
-#endif
 // Born fields of forward group grp: [group_begin(grp), group_begin(grp + 1)), G near-equal groups.
 __device__ __forceinline__ int group_begin(int K, int G, int grp) { return (K * grp) / G; }
 
@@ -360,15 +354,9 @@ struct FwdProducer {  // thread 0's walk over this CTA's items (decoded once per
   }
   __device__ __forceinline__ void decode(const FwdParams& p) {
     if (u >= U) return;
-#if HV_UNIT_ORDER_GST
     const int grp = u / (p.S * ntl);
     const int rem = u - grp * p.S * ntl;
     const int s = rem / ntl, tile = rem - s * ntl;
-#else
-    const int s = u / (p.G * ntl);
-    const int rem = u - s * p.G * ntl;
-    const int grp = rem / ntl, tile = rem - grp * ntl;
-#endif
     const int by = tile / p.g.ntx;
     x0 = (tile - by * p.g.ntx) * TX, z0 = by * TZ;
     fb = group_begin(p.K, p.G, grp);
@@ -469,12 +457,7 @@ __device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages
       for (int i = 0; i < 4; ++i)
         if (J0 + i >= g.Nx) v[i] = 0.0f;
     }
-#if HV_ST_HINT
-    if (row_ok[r])
-      st4_hint(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]), prod.pol_first);
-#else
     if (row_ok[r]) st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
-#endif
   };
 
   // ---------------- background u of shot s: L u^n (kept for the Born sources), leader updates u
@@ -596,15 +579,9 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
     for (int i = 0; i < NSTAGE_F; ++i) prod.issue(p);
   RingF cons;
   for (int u = blockIdx.x; u < U; u += nstep) {
-#if HV_UNIT_ORDER_GST
     const int grp = u / (p.S * ntl);
     const int rem = u - grp * p.S * ntl;
     const int s = rem / ntl, tile = rem - s * ntl;
-#else
-    const int s = u / (p.G * ntl);
-    const int rem = u - s * p.G * ntl;
-    const int grp = rem / ntl, tile = rem - grp * ntl;
-#endif
     const int bx = tile % p.g.ntx, by = tile / p.g.ntx;
     if (tile_is_interior(p.g, bx * TX, by * TZ))
       fwd_unit<false>(p, stages, bars, s, grp, bx, by, cons, prod);
@@ -656,8 +633,6 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   if (nf <= 0 || se <= sb) return;
   const int nitems = (se - sb) * nf;
   const int par_in = (p.j + 1) & (p.nlev - 1), par_out = p.j & (p.nlev - 1);
-  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
-  (void)pol_last;
   int ps = sb, pt = 0, issued = 0;
   Ring prod;
   auto issue_next = [&]() {
@@ -665,11 +640,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
     const int pl = (ps * p.nslot + p.slot0 + fb + pt) * p.nlev;
     mbar_expect_tx(&bars[prod.stage], TILE_BYTES + (p.update ? PT_BYTES : 0));
     tma_load_3d(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_in);
-#if HV_BWD_HINTS
-    if (p.update) tma_load_3d_hint(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_out, pol_first);
-#else
     if (p.update) tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_out);
-#endif
     prod.advance();
     if (++pt == nf) {
       pt = 0;
@@ -704,14 +675,8 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
 #pragma unroll
     for (int r = 0; r < RZ; ++r) {
       dst[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-#if HV_BWD_HINTS
-      if (img_rows[r])
-        dst[r] = ldg4_hint(p.s_lvl + s * p.s_shot_stride + static_cast<long long>(I0 + r - g.W) * g.PI + jc,
-                           pol_first);
-#else
       if (img_rows[r])
         dst[r] = ldg4(p.s_lvl + s * p.s_shot_stride + static_cast<long long>(I0 + r - g.W) * g.PI + jc);
-#endif
     }
   };
   float4 snext[RZ];
@@ -730,9 +695,6 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
       for (int i = 0; i < 4; ++i) acc[t][r][i] = 0.0f;
 
   Ring cons;
-  Ring erel;          // HV_BWD_EMPTY: stage the next refill waits on
-  int consumed = 0;
-  (void)erel, (void)consumed;
   for (int s = sb; s < se; ++s) {
     float sj[RZ][4];
 #pragma unroll
@@ -775,12 +737,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
             for (int i = 0; i < 4; ++i)
               if (J0 + i >= g.Nx) v[i] = 0.0f;
           }
-#if HV_ST_HINT
-          if (row_ok[r])
-            st4_hint(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]), pol_first);
-#else
           if (row_ok[r]) st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
-#endif
         }
       }
       // zero-lag imaging, summed over the batch's shots in registers: acc += s^j * lambda^{j+1}
@@ -788,27 +745,12 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
       for (int r = 0; r < RZ; ++r)
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[t][r][i] = fmaf(sj[r][i], C[r][i], acc[t][r][i]);
-#if HV_BWD_EMPTY
-      // release the stage per warp (empty barrier); warp 0 refills the stage of the item before this one once
-      // every warp has released it. Only tiles with receivers need a block barrier: the injection below adds
-      // into points other warps store.
-      __syncwarp();
-      if ((tid & 31) == 0) mbar_arrive(&bars[NSTAGE + cons.stage]);
-      cons.advance();
-      if (tid == 0 && ++consumed >= 2) {
-        mbar_wait(&bars[NSTAGE + erel.stage], erel.phase);
-        erel.advance();
-        if (issued < nitems) issue_next();
-      }
-      if (p.update && re > rb) __syncthreads();  // lambda^j of this tile stored (uniform per CTA)
-#else
       __syncthreads();  // stage consumed and lambda^j of this tile stored
       cons.advance();
       if (tid == 0 && issued < nitems) {
         fence_proxy_async();
         issue_next();
       }
-#endif
       // receiver injection into lambda^j: += v^2 / (1 + c) * rho[j][r]   (R^T scatter-add)
       if (p.update && re > rb) {
         const int slot = p.slot0 + fb + t;
@@ -830,13 +772,8 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
 #pragma unroll
       for (int r = 0; r < RZ; ++r) {
         if (!img_rows[r]) continue;
-#if HV_BWD_HINTS
-        red4_hint(a + static_cast<long long>(r) * g.P,
-                  make_float4(acc[t][r][0], acc[t][r][1], acc[t][r][2], acc[t][r][3]), pol_last);
-#else
         atomicAdd(reinterpret_cast<float4*>(a + static_cast<long long>(r) * g.P),
                   make_float4(acc[t][r][0], acc[t][r][1], acc[t][r][2], acc[t][r][3]));
-#endif
       }
     }
   }
@@ -852,7 +789,6 @@ __global__ void __launch_bounds__(NTHREADS, HV_BWD_MINB)
     tma_prefetch_desc(&mh);
     tma_prefetch_desc(&mt);
     for (int i = 0; i < NSTAGE; ++i) mbar_init(&bars[i], 1);
-    for (int i = 0; i < NSTAGE; ++i) mbar_init(&bars[NSTAGE + i], NTHREADS / 32);
     fence_mbar_init();
   }
   __syncthreads();
@@ -892,7 +828,9 @@ __device__ __forceinline__ void rev_body(const CUtensorMap* mh, const CUtensorMa
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
   const int x0 = blockIdx.x * TX, z0 = blockIdx.y * TZ;
   const int par_j = p.j & 1, par_o = par_j ^ 1;
-  int issued = 0;
+  // grid.z splits the batch's shots: this CTA rebuilds shots [s0, s1)
+  const int s0 = (blockIdx.z * p.S) / gridDim.z, s1 = ((blockIdx.z + 1) * p.S) / gridDim.z;
+  int issued = s0;
   Ring prod;
   auto issue_next = [&]() {
     float* st = stages + prod.stage * STAGE_FLOATS;
@@ -904,7 +842,7 @@ __device__ __forceinline__ void rev_body(const CUtensorMap* mh, const CUtensorMa
     ++issued;
   };
   if (tid == 0) {
-    while (issued < min(NSTAGE, p.S)) issue_next();
+    while (issued < min(s0 + NSTAGE, s1)) issue_next();
   }
   const int I0 = z0 + ty * RZ;
   const int J0 = x0 + tx * 4;
@@ -926,7 +864,7 @@ __device__ __forceinline__ void rev_body(const CUtensorMap* mh, const CUtensorMa
   const float amp = p.src_amp[p.j];
   const int jc = J0 - g.c0;
   Ring cons;
-  for (int s = 0; s < p.S; ++s) {
+  for (int s = s0; s < s1; ++s) {
     const float* st = stages + cons.stage * STAGE_FLOATS;
     mbar_wait(&bars[cons.stage], cons.phase);
     float2 L2[RZ][2], C2[RZ][2];
@@ -971,7 +909,7 @@ __device__ __forceinline__ void rev_body(const CUtensorMap* mh, const CUtensorMa
     }
     __syncthreads();
     cons.advance();
-    if (tid == 0 && issued < p.S) {
+    if (tid == 0 && issued < s1) {
       fence_proxy_async();
       issue_next();
     }

@@ -1,4 +1,3 @@
-# A/B timing of launch/kernel variants on cfg 1 (dev tool): bash tools/gpu_variants.sh
-for v in split1 split4; do echo "== $v"; HV_LIB=build/libhv_$v.so python tools/tune.py --config 1 --S 16 --FG 16 --reps 2 2>&1 | tail -1; done
-echo "== split2"; python tools/tune.py --config 1 --S 16 --FG 16 --reps 2 2>&1 | tail -1
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q 2>&1 | tail -2
+# planner fix check: cfg2 bench line + whole GPU suite (dev tool)
+timeout 600 python bench.py --config 2 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/bench_cfg2b.json 2> gpurun_out/bench_cfg2b.err; echo cfg2=$?; tail -1 gpurun_out/bench_cfg2b.json
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pt.log 2>&1; echo pt=$?; tail -3 gpurun_out/pt.log

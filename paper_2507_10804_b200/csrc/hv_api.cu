@@ -135,10 +135,6 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
                                   " GB per shot in flight; budget " + std::to_string(budget / 1e9) + " GB");
   int S = c->cfg.shot_batch > 0 ? c->cfg.shot_batch : 0;
   const int ntiles = g.ntx * g.ntz;
-  // forward Born fields per unit (max; groups are near-equal): fewer groups = fewer background recomputes per
-  // shot and tile, more groups = finer load balance over the one-wave grid
-  pl->FG = std::min(FWD_FG_MAX, c->cfg.field_group > 0 ? c->cfg.field_group : 16);
-  (void)ntiles;
   if (S <= 0) S = 32;  // every CTA loops over the batch's shots: more shots amortise q_k loads and imaging writes
   S = std::min(S, fit);
   S = std::max(1, std::min(S, c->nloc));
@@ -147,6 +143,30 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
     S = (c->nloc + nb - 1) / nb;
   }
   pl->S = S;
+  // forward Born fields per unit (groups are near-equal): fewer groups = fewer background recomputes per shot and
+  // tile, more groups = finer load balance over the one-wave grid. Auto: the G minimising the busiest CTA's items,
+  // ceil(S G tiles / CTAs) * (1 + ceil(K / G)) (cfg 1: G = 4 at 16 shots per rank, G = 5 at 2 shots per rank).
+  if (c->cfg.field_group > 0 || K <= 0) {
+    pl->FG = std::min(FWD_FG_MAX, c->cfg.field_group > 0 ? c->cfg.field_group : 16);
+  } else {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fwd_step_kernel, BX * BY, fwd_smem_bytes(0)) !=
+            cudaSuccess || nb < 1) {
+      cudaGetLastError();
+      nb = 2;
+    }
+    const long long ncta = static_cast<long long>(nb) * c->nsm;
+    long long best = -1;
+    int bestG = 1;
+    for (int G = 1; G <= K; ++G) {
+      const int fg = (K + G - 1) / G;
+      if (fg > FWD_FG_MAX || (G > 1 && (K + G - 2) / (G - 1) == fg)) continue;  // same FG as G - 1
+      const long long units = static_cast<long long>(pl->S) * G * ntiles;
+      const long long cost = ((units + ncta - 1) / ncta) * (1 + fg);
+      if (best < 0 || cost < best) best = cost, bestG = G;
+    }
+    pl->FG = (K + bestG - 1) / bestG;
+  }
   // a plan that needs the memory the workspace holds releases it first (buffers are re-allocated at their new
   // sizes by this call; captured graphs refer to the old addresses and are dropped with them)
   if (!c->cfg.mem_budget && shared + pl->S * pl->per_shot > 0.9 * static_cast<double>(freeb) && held > 0) {

@@ -295,6 +295,9 @@ struct Damp<false> {
 };
 template <bool SP>
 using BwdDamp = Damp<SP>;
+#ifndef HV_BWD_PAIRED
+#define HV_BWD_PAIRED 1  // backward arithmetic on column pairs (FFMA2), like the forward
+#endif
 
 template <bool SP>
 __device__ __forceinline__ float dmp_ci(const Damp<SP>& d, int r, int i) {
@@ -656,6 +659,9 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   const int so = ty * RZ * TX + tx * 4;
   const long long go = static_cast<long long>(I0) * g.P + J0;
   const int jc = J0 - g.c0;
+#if HV_BWD_PAIRED
+  float2 w2[RZ][2];
+#endif
   float w[RZ][4];
   bool img_rows[RZ], row_ok[RZ];
   bool any_img = false;
@@ -664,6 +670,9 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
     const int I = I0 + r;
     const float4 wv = ldg4(p.W2 + static_cast<long long>(min(I, g.Nz - 1)) * g.P + J0);
     w[r][0] = wv.x, w[r][1] = wv.y, w[r][2] = wv.z, w[r][3] = wv.w;
+#if HV_BWD_PAIRED
+    w2[r][0] = lo2(wv), w2[r][1] = hi2(wv);
+#endif
     const int iz = I - g.W;
     img_rows[r] = p.imaging && iz >= 0 && iz < g.nz && J0 + 3 >= g.W && J0 < g.W + g.nx && jc >= 0 &&
                   jc < g.PI;
@@ -686,6 +695,13 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   const int tile_id = blockIdx.y * g.ntx + blockIdx.x;
   const int rb = p.trec_beg[tile_id], re = p.trec_beg[tile_id + 1];
   const long long data_stride = static_cast<long long>(g.nt) * g.nrec;
+#if HV_BWD_PAIRED
+  float2 acc[BWD_FG][RZ][2];
+#pragma unroll
+  for (int t = 0; t < BWD_FG; ++t)
+#pragma unroll
+    for (int r = 0; r < RZ; ++r) acc[t][r][0] = acc[t][r][1] = make_float2(0.0f, 0.0f);
+#else
   float acc[BWD_FG][RZ][4];
 #pragma unroll
   for (int t = 0; t < BWD_FG; ++t)
@@ -693,6 +709,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
     for (int r = 0; r < RZ; ++r)
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[t][r][i] = 0.0f;
+#endif
 
   Ring cons;
   for (int s = sb; s < se; ++s) {
@@ -713,6 +730,33 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
       const float* st = stages + cons.stage * STAGE_FLOATS;
       float* dst = out_base + static_cast<long long>(t) * p.nlev * g.plane;
       mbar_wait(&bars[cons.stage], cons.phase);
+#if HV_BWD_PAIRED
+      float2 L2[RZ][2], C2[RZ][2];
+      lap_points(st, tx, ty, L2, C2);
+      if (p.update) {
+#pragma unroll
+        for (int r = 0; r < RZ; ++r) {
+          const float4 pv = ld4(st + TILE_FLOATS + so + r * TX);
+          float v[4];
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const float2 uu = dmp.upd(r, hh, C2[r][hh], half2of(pv, hh), mul2(w2[r][hh], L2[r][hh]));
+            v[2 * hh] = uu.x, v[2 * hh + 1] = uu.y;
+          }
+          if (SP) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (J0 + i >= g.Nx) v[i] = 0.0f;
+          }
+          if (row_ok[r]) st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RZ; ++r) {
+        acc[t][r][0] = fma2(make_float2(sj[r][0], sj[r][1]), C2[r][0], acc[t][r][0]);
+        acc[t][r][1] = fma2(make_float2(sj[r][2], sj[r][3]), C2[r][1], acc[t][r][1]);
+      }
+#else
       float L[RZ][4], C[RZ][4];
       {
         float2 L2[RZ][2], C2[RZ][2];
@@ -745,6 +789,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
       for (int r = 0; r < RZ; ++r)
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[t][r][i] = fmaf(sj[r][i], C[r][i], acc[t][r][i]);
+#endif
       __syncthreads();  // stage consumed and lambda^j of this tile stored
       cons.advance();
       if (tid == 0 && issued < nitems) {
@@ -772,8 +817,13 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
 #pragma unroll
       for (int r = 0; r < RZ; ++r) {
         if (!img_rows[r]) continue;
+#if HV_BWD_PAIRED
+        atomicAdd(reinterpret_cast<float4*>(a + static_cast<long long>(r) * g.P),
+                  make_float4(acc[t][r][0].x, acc[t][r][0].y, acc[t][r][1].x, acc[t][r][1].y));
+#else
         atomicAdd(reinterpret_cast<float4*>(a + static_cast<long long>(r) * g.P),
                   make_float4(acc[t][r][0], acc[t][r][1], acc[t][r][2], acc[t][r][3]));
+#endif
       }
     }
   }

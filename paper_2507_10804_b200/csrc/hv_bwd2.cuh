@@ -240,7 +240,7 @@ __device__ __forceinline__ void bwd2_body(const CUtensorMap* mh, const CUtensorM
   }
 }
 
-__global__ void __launch_bounds__(NTHREADS, 2)
+__global__ void __launch_bounds__(NTHREADS, MINB)
     bwd2_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
                 const Bwd2Params p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];

@@ -304,7 +304,7 @@ __device__ __forceinline__ void fwd2_unit(const Fwd2Params& p, const float* stag
   }
 }
 
-__global__ void __launch_bounds__(NTHREADS, 2)
+__global__ void __launch_bounds__(NTHREADS, MINB)
     fwd2_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
                 const __grid_constant__ CUtensorMap mq, const Fwd2Params p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];

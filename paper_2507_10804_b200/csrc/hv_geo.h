@@ -5,11 +5,15 @@ namespace hvk {
 
 constexpr int R = 4;                 // stencil radius (8th order)
 constexpr int TX = 64;               // tile width  (x, contiguous)
-constexpr int TZ = 32;               // tile height (z)
+#ifndef HV_TZ
+#define HV_TZ 32
+#endif
+constexpr int TZ = HV_TZ;            // tile height (z)
 constexpr int BX = 16;               // threads along x, 4 consecutive points (one float4) each
-constexpr int BY = 16;               // threads along z
+constexpr int BY = TZ / 2;           // threads along z (2 rows each)
 constexpr int RZ = TZ / BY;          // consecutive rows per thread
 constexpr int NTHREADS = BX * BY;
+constexpr int MINB = NTHREADS >= 512 ? 1 : 2;  // resident CTAs per SM the register budget is sized for
 constexpr int HX = TX + 2 * R;       // halo tile width  (72 floats = 288 B, a multiple of 16 B for TMA)
 constexpr int HZ = TZ + 2 * R;       // halo tile height
 constexpr int TILE_FLOATS = HX * HZ;          // halo tile (stencil input)

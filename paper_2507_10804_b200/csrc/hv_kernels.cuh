@@ -550,10 +550,10 @@ __device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages
 }
 
 #ifndef HV_FWD_MINB
-#define HV_FWD_MINB 2
+#define HV_FWD_MINB MINB
 #endif
 #ifndef HV_BWD_MINB
-#define HV_BWD_MINB 2
+#define HV_BWD_MINB MINB
 #endif
 __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
     fwd_step_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
@@ -966,7 +966,7 @@ __device__ __forceinline__ void rev_body(const CUtensorMap* mh, const CUtensorMa
   }
 }
 
-__global__ void __launch_bounds__(NTHREADS, 2)
+__global__ void __launch_bounds__(NTHREADS, MINB)
     rev_step_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
                     const RevParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];

@@ -13,7 +13,7 @@ constexpr int BX = 16;               // threads along x, 4 consecutive points (o
 constexpr int BY = TZ / 2;           // threads along z (2 rows each)
 constexpr int RZ = TZ / BY;          // consecutive rows per thread
 constexpr int NTHREADS = BX * BY;
-constexpr int MINB = NTHREADS >= 512 ? 1 : 2;  // resident CTAs per SM the register budget is sized for
+constexpr int MINB = NTHREADS >= 512 ? 1 : 512 / NTHREADS;  // resident CTAs per SM the registers are sized for
 constexpr int HX = TX + 2 * R;       // halo tile width  (72 floats = 288 B, a multiple of 16 B for TMA)
 constexpr int HZ = TZ + 2 * R;       // halo tile height
 constexpr int TILE_FLOATS = HX * HZ;          // halo tile (stencil input)

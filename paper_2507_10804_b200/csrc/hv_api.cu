@@ -365,6 +365,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     fp.ring_shot_stride = ringN * g.nt;
     if (boundary && phase == 0) CU_TRY(cudaMemsetAsync(ring, 0, sizeof(float) * ringN * g.nt * Sb, c->stream));
     fp.G = Gf;
+    fp.tile_major = 4.0 * K * g.plane > 48e6 ? 1 : 0;  // Q no longer L2-resident across a group's shots
     const dim3 gridf(fwd_grid(ntiles_all * Gf * Sb));
     if (phase == 0 && use_t2) {
       Fwd2Params f2{};

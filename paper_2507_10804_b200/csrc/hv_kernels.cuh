@@ -237,7 +237,8 @@ struct FwdParams {
   int born_slot0;         // Born field k lives in slot born_slot0 + k
   int K;                  // Born fields
   int S;                  // shots of the batch
-  int G;                  // Born-field groups (near-equal sizes, group_begin); work unit = (shot, group, tile)
+  int G;                  // Born-field groups (near-equal sizes, group_begin); work unit = (group, shot, tile)
+  int tile_major;         // unit order (group, tile, shot) instead (fwd_unit_decode)
   const float* W2;        // [Nz][P]   dt^2 v^2 / h^2 (0 outside the padded grid)
   const float* imgc;      // [nz][PI]  2 dt^2 / (v h^2); with s_out: store s^n = imgc * Lu^n
   float* s_out;           // level-n slot of the imaging-factor store for s_local = 0, or null
@@ -332,6 +333,20 @@ using RingF = RingN<NSTAGE_F>;  // forward kernel
 #ifndef HV_FWD_EMPTY
 #define HV_FWD_EMPTY 1  // forward: per-stage empty mbarriers instead of a block barrier per item
 #endif
+// Forward unit u -> (group, shot, tile). Order (group, shot, tile) keeps the resident CTAs on neighbouring tiles
+// of one shot (halo and background reads hit L2) and a group's q_k tiles L2-resident while they fit; with
+// p.tile_major the order is (group, tile, shot): a (group, tile)'s shots run on neighbouring CTAs at the same
+// time, so each q_k tile is read once per launch whatever the grid size (the host picks it when Q > 48 MB).
+__device__ __forceinline__ void fwd_unit_decode(const FwdParams& p, int u, int ntl, int& grp, int& s, int& tile) {
+  grp = u / (p.S * ntl);
+  const int rem = u - grp * p.S * ntl;
+  if (p.tile_major) {
+    tile = rem / p.S, s = rem - tile * p.S;
+  } else {
+    s = rem / ntl, tile = rem - s * ntl;
+  }
+}
+
 // Born fields of forward group grp: [group_begin(grp), group_begin(grp + 1)), G near-equal groups.
 __device__ __forceinline__ int group_begin(int K, int G, int grp) { return (K * grp) / G; }
 
@@ -357,9 +372,8 @@ struct FwdProducer {  // thread 0's walk over this CTA's items (decoded once per
   }
   __device__ __forceinline__ void decode(const FwdParams& p) {
     if (u >= U) return;
-    const int grp = u / (p.S * ntl);
-    const int rem = u - grp * p.S * ntl;
-    const int s = rem / ntl, tile = rem - s * ntl;
+    int grp, s, tile;
+    fwd_unit_decode(p, u, ntl, grp, s, tile);
     const int by = tile / p.g.ntx;
     x0 = (tile - by * p.g.ntx) * TX, z0 = by * TZ;
     fb = group_begin(p.K, p.G, grp);
@@ -582,9 +596,8 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
     for (int i = 0; i < NSTAGE_F; ++i) prod.issue(p);
   RingF cons;
   for (int u = blockIdx.x; u < U; u += nstep) {
-    const int grp = u / (p.S * ntl);
-    const int rem = u - grp * p.S * ntl;
-    const int s = rem / ntl, tile = rem - s * ntl;
+    int grp, s, tile;
+    fwd_unit_decode(p, u, ntl, grp, s, tile);
     const int bx = tile % p.g.ntx, by = tile / p.g.ntx;
     if (tile_is_interior(p.g, bx * TX, by * TZ))
       fwd_unit<false>(p, stages, bars, s, grp, bx, by, cons, prod);

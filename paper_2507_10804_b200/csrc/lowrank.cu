@@ -20,10 +20,6 @@ namespace {
 
 int grid_for(long long n) { return static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16)); }
 
-__global__ void f32_to_z(long long n, const float* __restrict__ a, cufftDoubleComplex* __restrict__ z) {
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x)
-    z[q] = make_cuDoubleComplex(static_cast<double>(a[q]), 0.0);
-}
 __global__ void d_to_z(long long n, const double* __restrict__ a, cufftDoubleComplex* __restrict__ z) {
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x)
     z[q] = make_cuDoubleComplex(a[q], 0.0);

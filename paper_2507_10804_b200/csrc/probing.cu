@@ -13,7 +13,6 @@ using namespace hvrt;
 
 namespace {
 
-constexpr float kPi = 3.14159265358979323846f;
 
 int grid_for(long long n) { return static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16)); }
 

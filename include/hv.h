@@ -75,10 +75,12 @@ typedef struct {
   int32_t src_begin, src_end; /* this rank's shot shard [begin, end); end = 0 means nsrc                  */
   int32_t store;         /* HV_STORE_* (AUTO: FULL if it fits, else CHECKPOINT)                         */
   int32_t ckpt_interval; /* CHECKPOINT spacing in levels; 0 = round(sqrt(nt))                            */
-  int32_t shot_batch;    /* shots propagated concurrently; 0 = auto from the memory budget               */
-  int32_t field_group;   /* max Born fields per forward work unit (tuning); 0 = auto (16)                 */
+  int32_t shot_batch;    /* shots propagated concurrently; 0 = auto: the most that fit the budget (<= 32),
+                            then ceil(nshard / S) near-equal batches                                      */
+  int32_t field_group;   /* max Born fields per forward work unit (tuning); 0 = auto (busiest-CTA model)   */
   int32_t device;        /* CUDA device ordinal                                                          */
-  size_t  mem_budget;    /* bytes of device memory the plan may use; 0 = 90 % of free memory             */
+  size_t  mem_budget;    /* bytes of device memory the plan may use; 0 = 90 % of (free memory + the
+                            context's own H.v workspace, which a larger plan releases and re-allocates)   */
 } hv_config;
 
 /* Create / destroy. Validates geometry (indices inside the interior grid) -> HV_EINVAL. */
@@ -177,7 +179,7 @@ typedef struct {
   int64_t kernel_launches;   /* launches of this library's kernels in the last call           */
   int64_t graph_launches;    /* CUDA-graph replays in the last call                           */
   int32_t shot_batch;        /* shots in flight used                                          */
-  int32_t field_group;       /* fields per CTA used                                           */
+  int32_t field_group;       /* max Born fields per forward work unit used                    */
   int32_t store;             /* storage mode used                                             */
   int32_t ckpt_interval;
   double  bytes_per_shot;    /* device bytes per shot in flight                               */

@@ -193,6 +193,23 @@ def test_two_step_kernels_bitwise_equal_single_step(hv, ragged, nt, monkeypatch)
         assert rel_l2(h1, HV) <= TOL
 
 
+@pytest.mark.parametrize("nz,nx,ns,K,fg,batch", [
+    (5, 200, 3, 7, 3, 1),      # a one-tile-row grid, 7 Born fields in near-equal groups of <= 3, 1 shot per batch
+    (150, 7, 2, 17, 0, 0),     # a one-tile-column grid, auto field groups (busiest-CTA model) for K = 17
+    (40, 300, 5, 1, 0, 2),     # K = 1, 5 shots in batches of 2 (ragged last batch)
+])
+def test_schedule_shapes(hv, nz, nx, ns, K, fg, batch):
+    """Forward one-wave schedule and backward grid on degenerate shapes: thin grids, K not a multiple of the group
+    size, a single probe, ragged shot batches -- H·v against the oracle."""
+    wl = W.custom(nz, nx, nt=120, ns=ns, nrec=max(2, nx // 3), n_probes=K, f_peak=20.0, seed=3)
+    V = wl.probes()
+    ref = wave.Problem(wl).hessvec(list(V.astype(np.float64)))
+    out = hv.Solver.from_workload(wl, shot_batch=batch, field_group=fg).hessvec(wl.model, V)
+    assert rel_l2(out, ref) <= TOL
+    for k in range(K):
+        assert rel_l2(out[k], ref[k]) <= TOL
+
+
 def test_edge_cases(hv):
     # degenerate: zero probe -> zero H v, zero residual -> zero gradient; minimum grid; receiver on a corner
     wl = W.custom(1, 5, nt=40, ns=1, nrec=2, n_probes=1, W=4, f_peak=25.0, seed=2)

@@ -366,6 +366,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     if (boundary && phase == 0) CU_TRY(cudaMemsetAsync(ring, 0, sizeof(float) * ringN * g.nt * Sb, c->stream));
     fp.G = Gf;
     fp.tile_major = 4.0 * K * g.plane > 48e6 ? 1 : 0;  // Q no longer L2-resident across a group's shots
+    if (const char* uo = std::getenv("HV_UNIT_ORDER"))  // tuning override: "gst" | "gts"
+      fp.tile_major = std::strcmp(uo, "gts") == 0 ? 1 : 0;
     const dim3 gridf(fwd_grid(ntiles_all * Gf * Sb));
     if (phase == 0 && use_t2) {
       Fwd2Params f2{};

@@ -1,5 +1,3 @@
-# backward fields per CTA at small per-rank shot counts (dev tool)
-for sh in 2 4; do
-echo "== default shots $sh"; python tools/tune.py --config 1 --shots $sh --S 16 --FG 0 --reps 2 2>&1 | tail -1
-for v in 3 4; do echo "== bfg$v shots $sh"; HV_LIB=build/libhv_bfg$v.so python tools/tune.py --config 1 --shots $sh --S 16 --FG 0 --reps 2 2>&1 | tail -1; done
-done
+# unit order on cfg3 (Q = 66 MB) and cfg2 (dev tool)
+for o in gst gts; do echo "== cfg3 $o"; HV_UNIT_ORDER=$o python tools/tune.py --config 3 --shots 16 --S 16 --FG 0 --reps 1 2>&1 | tail -1; done
+for o in gst gts; do echo "== cfg2 $o"; HV_UNIT_ORDER=$o python tools/tune.py --config 2 --shots 22 --S 22 --FG 0 --reps 1 2>&1 | tail -1; done

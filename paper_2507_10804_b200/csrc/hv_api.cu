@@ -365,9 +365,11 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     fp.ring_shot_stride = ringN * g.nt;
     if (boundary && phase == 0) CU_TRY(cudaMemsetAsync(ring, 0, sizeof(float) * ringN * g.nt * Sb, c->stream));
     fp.G = Gf;
-    fp.tile_major = 4.0 * K * g.plane > 48e6 ? 1 : 0;  // Q no longer L2-resident across a group's shots
-    if (const char* uo = std::getenv("HV_UNIT_ORDER"))  // tuning override: "gst" | "gts"
-      fp.tile_major = std::strcmp(uo, "gts") == 0 ? 1 : 0;
+    // unit order: one shot per block while Q stays L2-resident; otherwise as many shots per block as keep the
+    // resident window (~296 units) at two tile rows or more
+    fp.sblk = 1;
+    if (4.0 * K * g.plane > 48e6) fp.sblk = std::min(Sb, std::max(2, 296 / std::max(1, 2 * g.ntx)));
+    if (const char* sbe = std::getenv("HV_SBLK")) fp.sblk = std::max(1, std::min(Sb, std::atoi(sbe)));  // tuning
     const dim3 gridf(fwd_grid(ntiles_all * Gf * Sb));
     if (phase == 0 && use_t2) {
       Fwd2Params f2{};

@@ -238,7 +238,7 @@ struct FwdParams {
   int K;                  // Born fields
   int S;                  // shots of the batch
   int G;                  // Born-field groups (near-equal sizes, group_begin); work unit = (group, shot, tile)
-  int tile_major;         // unit order (group, tile, shot) instead (fwd_unit_decode)
+  int sblk;               // shots per block of the unit order (fwd_unit_decode), 1 <= sblk <= S
   const float* W2;        // [Nz][P]   dt^2 v^2 / h^2 (0 outside the padded grid)
   const float* imgc;      // [nz][PI]  2 dt^2 / (v h^2); with s_out: store s^n = imgc * Lu^n
   float* s_out;           // level-n slot of the imaging-factor store for s_local = 0, or null
@@ -333,18 +333,19 @@ using RingF = RingN<NSTAGE_F>;  // forward kernel
 #ifndef HV_FWD_EMPTY
 #define HV_FWD_EMPTY 1  // forward: per-stage empty mbarriers instead of a block barrier per item
 #endif
-// Forward unit u -> (group, shot, tile). Order (group, shot, tile) keeps the resident CTAs on neighbouring tiles
-// of one shot (halo and background reads hit L2) and a group's q_k tiles L2-resident while they fit; with
-// p.tile_major the order is (group, tile, shot): a (group, tile)'s shots run on neighbouring CTAs at the same
-// time, so each q_k tile is read once per launch whatever the grid size (the host picks it when Q > 48 MB).
+// Forward unit u -> (group, shot, tile). Units are ordered (group, shot block, tile, shot within the block) with
+// blocks of p.sblk shots: the resident window of ~296 units then covers 296 / sblk tiles x sblk shots. sblk = 1
+// keeps the window on neighbouring tiles of one shot (vertical halo overlaps and the background tile are L2 hits;
+// a group's q_k tiles stay L2-resident while Q fits), larger sblk shares each q_k tile among the window's
+// shots (Q larger than L2) as long as the window still spans a tile row (sblk <= 296 / ntx).
 __device__ __forceinline__ void fwd_unit_decode(const FwdParams& p, int u, int ntl, int& grp, int& s, int& tile) {
   grp = u / (p.S * ntl);
   const int rem = u - grp * p.S * ntl;
-  if (p.tile_major) {
-    tile = rem / p.S, s = rem - tile * p.S;
-  } else {
-    s = rem / ntl, tile = rem - s * ntl;
-  }
+  const int blk = rem / (p.sblk * ntl);
+  const int rem2 = rem - blk * p.sblk * ntl;
+  const int nb = min(p.sblk, p.S - blk * p.sblk);  // shots in this block (the last one may be short)
+  tile = rem2 / nb;
+  s = blk * p.sblk + (rem2 - tile * nb);
 }
 
 // Born fields of forward group grp: [group_begin(grp), group_begin(grp + 1)), G near-equal groups.

@@ -210,6 +210,20 @@ def test_schedule_shapes(hv, nz, nx, ns, K, fg, batch):
         assert rel_l2(out[k], ref[k]) <= TOL
 
 
+def test_unit_order_shot_blocks_bitwise(hv, monkeypatch):
+    """The forward unit order (shot blocks of HV_SBLK shots, a ragged last block) only reorders independent
+    items: d and H·v are bitwise equal for every block size."""
+    wl = W.custom(70, 150, nt=160, ns=5, nrec=30, n_probes=5, f_peak=15.0, seed=9)
+    V = wl.probes()
+    res = []
+    for b in ("1", "3", "5"):
+        monkeypatch.setenv("HV_SBLK", b)
+        s = hv.Solver.from_workload(wl, shot_batch=5, field_group=2)
+        res.append((s.forward(wl.model), s.hessvec(wl.model, V)))
+    for d, h in res[1:]:
+        assert np.array_equal(d, res[0][0]) and np.array_equal(h, res[0][1])
+
+
 def test_edge_cases(hv):
     # degenerate: zero probe -> zero H v, zero residual -> zero gradient; minimum grid; receiver on a corner
     wl = W.custom(1, 5, nt=40, ns=1, nrec=2, n_probes=1, W=4, f_peak=25.0, seed=2)

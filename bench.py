@@ -287,7 +287,7 @@ def main():
             torch.cuda.current_stream().synchronize()
         e2e_step()
         et = []
-        for _ in range(max(2, min(args.steps, 3))):
+        for _ in range(max(3, args.steps)):
             flush.fill_(1.0)
             torch.cuda.synchronize()
             if ws > 1:

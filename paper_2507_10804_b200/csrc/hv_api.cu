@@ -48,6 +48,7 @@ int make_tmap(hv_ctx* c, const float* base, long long nplanes, int box_w, int bo
 }
 
 constexpr bool kTwoStepDefault = false;
+constexpr int kQresFG = 6;  // resident-q forward: Born fields per CTA (6 q_k tiles + 3 stages: 2 CTAs per SM)
 // Backward CTAs per (tile, field group): the batch's shots are split into this many parts, each summing its
 // imaging terms into its own accumulator copy (finalize adds the copies in a fixed order). 2 halves the last
 // partial wave of the backward grid at the cost of one more RED per point and field per launch; measured on
@@ -371,6 +372,13 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     if (4.0 * K * g.plane > 48e6) fp.sblk = std::min(Sb, std::max(2, 296 / std::max(1, 2 * g.ntx)));
     if (const char* sbe = std::getenv("HV_SBLK")) fp.sblk = std::max(1, std::min(Sb, std::atoi(sbe)));  // tuning
     const dim3 gridf(fwd_grid(ntiles_all * Gf * Sb));
+    // resident-q forward (q_k read once per launch) for Q too large for L2: HV_QRES=0/1 overrides (tuning)
+    bool qres = K > 0 && 4.0 * K * g.plane > 48e6;
+    if (const char* qe = std::getenv("HV_QRES")) qres = K > 0 && std::strcmp(qe, "0") != 0;
+    fp.qfg = std::min(K > 0 ? K : 1, kQresFG);
+    if (const char* qf = std::getenv("HV_QFG")) fp.qfg = std::max(1, std::min({K > 0 ? K : 1, 16, std::atoi(qf)}));
+    const int Gq = K > 0 ? (K + fp.qfg - 1) / fp.qfg : 1;
+    const int qres_smem = STAGES_BYTES + BAR_BYTES + fp.qfg * PT_BYTES;
     if (phase == 0 && use_t2) {
       Fwd2Params f2{};
       f2.g = g;
@@ -421,7 +429,10 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
         fp.n = n;
         fp.s_out = full ? store + (size_t)n * g.iplane : nullptr;
         fp.ring_out = boundary ? ring + (size_t)(n + 1) * ringN : nullptr;
-        fwd_step_kernel<<<gridf, block, fwd_smem, c->stream>>>(map_halo, map_tile, map_q, fp);
+        if (qres)
+          fwd_qres_kernel<<<dim3(g.ntx, g.ntz, Gq), block, qres_smem, c->stream>>>(map_halo, map_tile, map_q, fp);
+        else
+          fwd_step_kernel<<<gridf, block, fwd_smem, c->stream>>>(map_halo, map_tile, map_q, fp);
         launches++;
       }
     }
@@ -834,6 +845,8 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
           cudaSuccess ||
       cudaFuncSetAttribute(bwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_BYTES) !=
           cudaSuccess ||
+      cudaFuncSetAttribute(fwd_qres_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           STAGES_BYTES + BAR_BYTES + 16 * PT_BYTES) != cudaSuccess ||
       cudaFuncSetAttribute(fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, F2_SMEM_BYTES) != cudaSuccess ||
       cudaFuncSetAttribute(bwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, B2_SMEM_BYTES) != cudaSuccess ||
       cudaFuncSetAttribute(rev_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_BYTES) !=

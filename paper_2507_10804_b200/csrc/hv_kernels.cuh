@@ -239,6 +239,7 @@ struct FwdParams {
   int S;                  // shots of the batch
   int G;                  // Born-field groups (near-equal sizes, group_begin); work unit = (group, shot, tile)
   int sblk;               // shots per block of the unit order (fwd_unit_decode), 1 <= sblk <= S
+  int qfg;                // fwd_qres_kernel: Born fields per CTA (q_k tiles resident in shared memory)
   const float* W2;        // [Nz][P]   dt^2 v^2 / h^2 (0 outside the padded grid)
   const float* imgc;      // [nz][PI]  2 dt^2 / (v h^2); with s_out: store s^n = imgc * Lu^n
   float* s_out;           // level-n slot of the imaging-factor store for s_local = 0, or null
@@ -605,6 +606,215 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
     else
       fwd_unit<true>(p, stages, bars, s, grp, bx, by, cons, prod);
   }
+}
+
+// ------------------------------------------------------------------------------------------------ forward, resident q
+// Forward for large Q (the v3 schedule, kept for grids whose Q does not fit L2): one CTA per (tile, Born group)
+// loops over all the batch's shots; the group's q_k tiles are loaded into shared memory once and reused by every
+// shot (q_k is read from DRAM once per launch), the resident CTAs step through the shots in lockstep (halo
+// overlaps are L2 hits). Scalar arithmetic, a block barrier per item, 3-stage ring of halo + level n-1 tiles.
+__device__ __forceinline__ void lap_points_scalar(const float* __restrict__ t, int tx, int ty, float (&L)[RZ][4],
+                                                  float (&C)[RZ][4]) {
+  float2 L2[RZ][2], C2[RZ][2];
+  lap_points(t, tx, ty, L2, C2);
+#pragma unroll
+  for (int r = 0; r < RZ; ++r)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      L[r][2 * h] = L2[r][h].x, L[r][2 * h + 1] = L2[r][h].y;
+      C[r][2 * h] = C2[r][h].x, C[r][2 * h + 1] = C2[r][h].y;
+    }
+}
+
+template <bool SP>
+__device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUtensorMap* mt, const CUtensorMap* mq,
+                                         const FwdParams& p, float* stages, float* qs, uint64_t* bars) {
+  const Geo& g = p.g;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
+  const int x0 = blockIdx.x * TX, z0 = blockIdx.y * TZ;
+  const int grp = blockIdx.z;
+  const int fb = grp * p.qfg;
+  const int nf = max(0, min(p.K, fb + p.qfg) - fb);   // Born fields of this CTA
+  const int nitems = p.S * (1 + nf);                  // per shot: background, then its Born fields
+  const int par_n = p.n & 1, par_new = par_n ^ 1;
+  const bool leader = (grp == 0) && p.bg_update;
+  uint64_t* qbar = bars + NSTAGE;
+
+  // producer (thread 0): next item (ps, pt) -> stage
+  int ps = 0, pt = 0, issued = 0;
+  Ring prod;
+  auto issue_next = [&]() {
+    float* st = stages + prod.stage * STAGE_FLOATS;
+    const bool upd = pt > 0 || leader;
+    const int slot = pt == 0 ? p.bg_slot : p.born_slot0 + fb + pt - 1;
+    const int pl = (ps * p.nslot + slot) * 2;
+    mbar_expect_tx(&bars[prod.stage], TILE_BYTES + (upd ? PT_BYTES : 0));
+    tma_load_3d(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_n);
+    if (upd) tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_new);
+    prod.advance();
+    if (++pt > nf) {
+      pt = 0;
+      ++ps;
+    }
+    ++issued;
+  };
+  if (tid == 0) {
+    if (nf > 0) {  // q_k tiles of the group, once for all shots
+      mbar_expect_tx(qbar, nf * PT_BYTES);
+      for (int t = 0; t < nf; ++t) tma_load_3d(qs + t * PT_FLOATS, mq, qbar, x0, z0, fb + t);
+    }
+    while (issued < min(NSTAGE, nitems)) issue_next();
+  }
+
+  const int I0 = z0 + ty * RZ;
+  const int J0 = x0 + tx * 4;
+  const int so = ty * RZ * TX + tx * 4;                       // smem offset of this thread's first point
+  const long long go = static_cast<long long>(I0) * g.P + J0;  // plane offset of this thread's first point
+  float w[RZ][4];
+#pragma unroll
+  for (int r = 0; r < RZ; ++r) {
+    const float4 wv = ldg4(p.W2 + static_cast<long long>(min(I0 + r, g.Nz - 1)) * g.P + J0);
+    w[r][0] = wv.x, w[r][1] = wv.y, w[r][2] = wv.z, w[r][3] = wv.w;
+  }
+  bool row_ok[RZ];
+#pragma unroll
+  for (int r = 0; r < RZ; ++r) row_ok[r] = !SP || I0 + r < g.Nz;
+  Damp<SP> dmp;
+  dmp.init(g, I0, J0);
+  const int tile_id = blockIdx.y * g.ntx + blockIdx.x;
+  const int rb = p.trec_beg[tile_id], re = p.trec_beg[tile_id + 1];
+  const float amp = p.src_amp[p.n];
+  const long long data_stride = static_cast<long long>(g.nt) * g.nrec;
+  if (nf > 0) mbar_wait(qbar, 0);
+
+  Ring cons;
+  auto release = [&]() {
+    __syncthreads();  // every thread is done with this stage
+    cons.advance();
+    if (tid == 0 && issued < nitems) {
+      fence_proxy_async();
+      issue_next();
+    }
+  };
+  auto sample = [&](const float* st, float* out) {  // d[n][r] = field^n[rec_r] from the staged tile
+    for (int q = rb + tid; q < re; q += NTHREADS) {
+      const int rid = p.trec_id[q];
+      const int lz = p.rec_I[rid] - z0 + R, lx = p.rec_J[rid] - x0 + R;
+      out[static_cast<long long>(p.n) * g.nrec + rid] = st[lz * HX + lx];
+    }
+  };
+  auto store_row = [&](float* dst, int r, float (&v)[4]) {
+    if (SP) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (J0 + i >= g.Nx) v[i] = 0.0f;
+    }
+    if (row_ok[r]) st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
+  };
+
+  float Lb[RZ][4];
+  for (int s = 0; s < p.S; ++s) {
+    // ---------------- background u of shot s: L u^n (kept for the Born sources), leader updates u
+    {
+      const float* st = stages + cons.stage * STAGE_FLOATS;
+      mbar_wait(&bars[cons.stage], cons.phase);
+      float C[RZ][4];
+      lap_points_scalar(st, tx, ty, Lb, C);
+      if (leader) {
+        float* dst = p.pool + (static_cast<long long>(s * p.nslot + p.bg_slot) * 2 + par_new) * g.plane;
+        const int sI = p.src_I[p.shot0 + s], sJ = p.src_J[p.shot0 + s];
+#pragma unroll
+        for (int r = 0; r < RZ; ++r) {
+          const float4 pv = ld4(st + TILE_FLOATS + so + r * TX);
+          float v[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[i] = dmp.upd1(r, i, C[r][i], f4(pv, i), w[r][i] * Lb[r][i]);
+          if (I0 + r == sI && sJ >= J0 && sJ < J0 + 4) {  // point source dt^2 s[n] / h^2 (/(1 + c))
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (J0 + i == sJ) v[i] += amp * dmp_ci(dmp, r, i);
+          }
+          if (SP && p.ring_out != nullptr) {  // BOUNDARY store: the ring of u^{n+1}
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int q = ring_index(g, I0 + r, J0 + i);
+              if (q >= 0) p.ring_out[s * p.ring_shot_stride + q] = v[i];
+            }
+          }
+          store_row(dst, r, v);
+        }
+        // imaging-factor store s^n = 2 dt^2 / (v h^2) * L~u^n on the interior (FULL store / replay segments)
+        const int jc = J0 - g.c0;
+        if (p.s_out != nullptr && jc >= 0 && jc < g.PI) {
+#pragma unroll
+          for (int r = 0; r < RZ; ++r) {
+            const int iz = I0 + r - g.W;
+            if (iz < 0 || iz >= g.nz) continue;
+            const float4 ic = ldg4(p.imgc + static_cast<long long>(iz) * g.PI + jc);
+            float o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int ix = J0 + i - g.W;
+              o[i] = (!SP || (ix >= 0 && ix < g.nx)) ? f4(ic, i) * Lb[r][i] : 0.0f;
+            }
+            st4(p.s_out + s * p.s_shot_stride + static_cast<long long>(iz) * g.PI + jc,
+                make_float4(o[0], o[1], o[2], o[3]));
+          }
+        }
+        if (re > rb && p.d_bg) sample(st, p.d_bg + (p.dbg_shot0 + s) * data_stride);
+      }
+      release();
+    }
+    // ---------------- Born fields du_k of shot s: source q_k L u^n
+    float* born_base = p.pool + (static_cast<long long>(s * p.nslot + p.born_slot0 + fb) * 2 + par_new) * g.plane;
+    for (int t = 0; t < nf; ++t) {
+      const float* st = stages + cons.stage * STAGE_FLOATS;
+      mbar_wait(&bars[cons.stage], cons.phase);
+      float L[RZ][4], C[RZ][4];
+      lap_points_scalar(st, tx, ty, L, C);
+      float* dst = born_base + static_cast<long long>(t) * 2 * g.plane;
+      const float* qk = qs + t * PT_FLOATS + so;
+#pragma unroll
+      for (int r = 0; r < RZ; ++r) {
+        const float4 pv = ld4(st + TILE_FLOATS + so + r * TX);
+        const float4 qv = ld4(qk + r * TX);
+        float v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          v[i] = dmp.upd1(r, i, C[r][i], f4(pv, i), fmaf(f4(qv, i), Lb[r][i], w[r][i] * L[r][i]));
+        store_row(dst, r, v);
+      }
+      if (re > rb && p.d_born) sample(st, p.d_born + (static_cast<long long>(s) * p.K + fb + t) * data_stride);
+      release();
+    }
+  }
+}
+
+#ifndef HV_FWD_MINB
+#define HV_FWD_MINB 2
+#endif
+#ifndef HV_BWD_MINB
+#define HV_BWD_MINB 2
+#endif
+__global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
+    fwd_qres_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
+                    const __grid_constant__ CUtensorMap mq, const FwdParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stages = reinterpret_cast<float*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES_BYTES);
+  float* qs = reinterpret_cast<float*>(smem_raw + STAGES_BYTES + BAR_BYTES);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    tma_prefetch_desc(&mh);
+    tma_prefetch_desc(&mt);
+    tma_prefetch_desc(&mq);
+    for (int i = 0; i < NSTAGE + 1; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tile_is_interior(p.g, blockIdx.x * TX, blockIdx.y * TZ))
+    fwd_qres_body<false>(&mh, &mt, &mq, p, stages, qs, bars);
+  else
+    fwd_qres_body<true>(&mh, &mt, &mq, p, stages, qs, bars);
 }
 
 // ------------------------------------------------------------------------------------------------ backward

@@ -224,6 +224,21 @@ def test_unit_order_shot_blocks_bitwise(hv, monkeypatch):
         assert np.array_equal(d, res[0][0]) and np.array_equal(h, res[0][1])
 
 
+@pytest.mark.parametrize("store", ["full", "checkpoint", "boundary"])
+def test_resident_q_forward(hv, ragged, store, monkeypatch):
+    """The resident-q forward (chosen for Q larger than L2; forced here with HV_QRES=1) against the oracle and
+    against the one-wave forward."""
+    wl, V, d, HV, *_ = ragged
+    out = {}
+    for q in ("1", "0"):
+        monkeypatch.setenv("HV_QRES", q)
+        monkeypatch.setenv("HV_QFG", "2")
+        s = hv.Solver.from_workload(wl, store=store, shot_batch=2)
+        out[q] = (s.forward(wl.model), s.hessvec(wl.model, V))
+    assert rel_l2(out["1"][0], d) <= TOL and rel_l2(out["1"][1], HV) <= TOL
+    assert rel_l2(out["1"][0], out["0"][0]) <= 1e-6 and rel_l2(out["1"][1], out["0"][1]) <= 1e-6
+
+
 def test_edge_cases(hv):
     # degenerate: zero probe -> zero H v, zero residual -> zero gradient; minimum grid; receiver on a corner
     wl = W.custom(1, 5, nt=40, ns=1, nrec=2, n_probes=1, W=4, f_peak=25.0, seed=2)

@@ -314,7 +314,9 @@ def main():
         f_launch_ms = float(np.mean(fwd_ms)) / (nbatch * (wl.nt - 1))
         b_launch_ms = float(np.mean(bwd_ms)) / (nbatch * (wl.nt - 1))
         peak, peak_src = hbm_peak()
-        kern = {"fwd_step_kernel": (fb, f_launch_ms), "bwd_step_kernel": (bb, b_launch_ms)}
+        fwd_name = {0: "fwd_step_kernel", 1: "fwd_qres_kernel", 2: "fwd2_kernel"}.get(solver.stats()["fwd_kernel"],
+                                                                                      "fwd_step_kernel")
+        kern = {fwd_name: (fb, f_launch_ms), "bwd_step_kernel": (bb, b_launch_ms)}
         dom = max(kern, key=lambda k: kern[k][1])
         achieved = kern[dom][0] / (kern[dom][1] / 1000.0) / 1e9
         traffic, traffic_src = None, None

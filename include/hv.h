@@ -186,6 +186,8 @@ typedef struct {
   double  ms_forward;        /* device time of the forward sweeps (CUDA events), last call    */
   double  ms_backward;       /* device time of the backward sweeps, last call                 */
   double  ms_total;          /* device time of the whole call                                 */
+  int32_t fwd_kernel;        /* forward sweep kernel used: 0 one-wave (fwd_step_kernel), 1 resident-q
+                                (fwd_qres_kernel, Q > 48 MB), 2 two-step (fwd2_kernel, HV_T2=1)  */
 } hv_stats;
 HV_API int hv_get_stats(const hv_ctx* ctx, hv_stats* out);
 

@@ -324,6 +324,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   // One shot batch = one enqueue of the whole time loop (forward sweep, checkpoint saves / replays, backward
   // sweep). It is captured once into a CUDA graph per (call signature, buffers) and replayed afterwards.
   int64_t batch_launches = 0;
+  int fwd_kernel_used = 0;
   // phase 0: forward sweep (+ gather); phase 1: backward sweep. Events may be null (recorded by the caller).
   auto enqueue_batch = [&](int phase, int b0, int Sb, cudaEvent_t e_f0, cudaEvent_t e_f1, cudaEvent_t e_b0,
                            cudaEvent_t e_b1) -> int {
@@ -379,6 +380,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     if (const char* qf = std::getenv("HV_QFG")) fp.qfg = std::max(1, std::min({K > 0 ? K : 1, 16, std::atoi(qf)}));
     const int Gq = K > 0 ? (K + fp.qfg - 1) / fp.qfg : 1;
     const int qres_smem = STAGES_BYTES + BAR_BYTES + fp.qfg * PT_BYTES;
+    fwd_kernel_used = use_t2 ? 2 : (qres ? 1 : 0);
     if (phase == 0 && use_t2) {
       Fwd2Params f2{};
       f2.g = g;
@@ -691,6 +693,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   c->stats.ms_forward = ms_f;
   c->stats.ms_backward = ms_b;
   c->stats.ms_total = tot;
+  c->stats.fwd_kernel = fwd_kernel_used;
   return HV_OK;
 }
 

@@ -58,6 +58,21 @@ constexpr int kQresFG = 6;  // resident-q forward: Born fields per CTA (6 q_k ti
 #endif
 constexpr int kBwdSplit = HV_BWD_SPLIT;
 
+// 3-D tensor map over interior planes [nplanes][nz][PI] (the imaging-factor stores), box TX x TZ.
+int make_tmap_interior(hv_ctx* c, const float* base, long long nplanes, CUtensorMap* map) {
+  const Geo& g = c->g;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.PI), static_cast<cuuint64_t>(g.nz),
+                        static_cast<cuuint64_t>(nplanes)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.PI) * 4, static_cast<cuuint64_t>(g.iplane) * 4};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(TX), static_cast<cuuint32_t>(TZ), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = c->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, HV_ECUDA, "cuTensorMapEncodeTiled (interior) failed: " + std::to_string(r));
+  return HV_OK;
+}
+
 int grid1d(long long n) { return static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16)); }
 
 // ------------------------------------------------------------------------------------------ the plan
@@ -288,6 +303,14 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   if ((st = make_tmap(c, pool, planes_per_shot * S, HX, HZ, &map_halo))) return st;
   if ((st = make_tmap(c, pool, planes_per_shot * S, TX, TZ, &map_tile))) return st;
   if ((st = make_tmap(c, Q ? Q : pool, Q ? K : planes_per_shot * S, TX, TZ, &map_q))) return st;
+  // s^j tensor map of the backward (FULL store / BOUNDARY level buffer / CHECKPOINT segment)
+  CUtensorMap map_sj = map_tile;
+  if (adjoint) {
+    if (pl.store == HV_STORE_FULL) st = make_tmap_interior(c, store, (long long)S * g.nt, &map_sj);
+    else if (pl.store == HV_STORE_BOUNDARY) st = make_tmap_interior(c, sbuf, 2LL * S, &map_sj);
+    else st = make_tmap_interior(c, seg, (long long)S * pl.k, &map_sj);
+    if (st) return st;
+  }
   if (phi_user) CU_TRY(cudaMemsetAsync(phi_d, 0, sizeof(double), c->stream));
 
   // --- the shot batches
@@ -549,13 +572,17 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
             rv.src_I = c->d_srcI;
             rv.src_J = c->d_srcJ;
             rv.src_amp = c->d_src_amp;
-            rev_step_kernel<<<dim3(g.ntx, g.ntz, Sb), block, BWD_SMEM_BYTES, c->stream>>>(map_halo, map_tile, rv);
+            rev_step_kernel<<<dim3(g.ntx, g.ntz, Sb), block, REV_SMEM_BYTES, c->stream>>>(map_halo, map_tile, rv);
             launches++;
             bp.s_lvl = rv.s_out;
             bp.s_shot_stride = g.iplane;
+            bp.sj_plane0 = (long long)(j & 1) * Sb;
+            bp.sj_shot_planes = 1;
           } else if (full) {
             bp.s_lvl = store + (size_t)j * g.iplane;
             bp.s_shot_stride = g.iplane * g.nt;
+            bp.sj_plane0 = j;
+            bp.sj_shot_planes = g.nt;
           } else {
             const int b = (j / pl.k) * pl.k;
             if (b != cur_b) {  // replay segment [b, e) of the background into the segment store
@@ -582,9 +609,11 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
             }
             bp.s_lvl = seg + (size_t)(j - cur_b) * g.iplane;
             bp.s_shot_stride = g.iplane * pl.k;
+            bp.sj_plane0 = j - cur_b;
+            bp.sj_shot_planes = pl.k;
           }
         }
-        bwd_step_kernel<<<gridb, block, BWD_SMEM_BYTES, c->stream>>>(map_halo, map_tile, bp);
+        bwd_step_kernel<<<gridb, block, BWD_SMEM_BYTES, c->stream>>>(map_halo, map_tile, map_sj, bp);
         launches++;
       }
       CU_TRY(cudaGetLastError());
@@ -852,7 +881,7 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
                            STAGES_BYTES + BAR_BYTES + 16 * PT_BYTES) != cudaSuccess ||
       cudaFuncSetAttribute(fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, F2_SMEM_BYTES) != cudaSuccess ||
       cudaFuncSetAttribute(bwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, B2_SMEM_BYTES) != cudaSuccess ||
-      cudaFuncSetAttribute(rev_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_BYTES) !=
+      cudaFuncSetAttribute(rev_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, REV_SMEM_BYTES) !=
           cudaSuccess) {
     cudaGetLastError();
     hv_destroy(c);

@@ -42,7 +42,11 @@ constexpr int FWD_FG_MAX = 64;
 constexpr int fwd_smem_bytes(int) { return FSTAGES_BYTES + BAR_BYTES; }
 // backward CTA: stages; its BWD_FG adjoint fields keep their imaging sums over the batch's shots in registers
 constexpr int BWD_FG = HV_BWD_FG;
-constexpr int BWD_SMEM_BYTES = STAGES_BYTES + BAR_BYTES;
+// backward stage: halo lambda^{j+1} + tile lambda^{j+2} + tile s^j (first field of a shot)
+constexpr int BSTAGE_FLOATS = TILE_FLOATS + 2 * PT_FLOATS;
+constexpr int BSTAGES_BYTES = NSTAGE * BSTAGE_FLOATS * 4;
+constexpr int BWD_SMEM_BYTES = BSTAGES_BYTES + BAR_BYTES;
+constexpr int REV_SMEM_BYTES = STAGES_BYTES + BAR_BYTES;  // BOUNDARY reverse kernel: halo + tile stages
 constexpr int B2_SMEM_BYTES = STAGES_BYTES + PT_FLOATS * 4 + BAR_BYTES;  // two-step adjoint: + mid
 
 // standard 8th-order central second-derivative weights (unscaled; h^-2 is folded into the coefficients)

@@ -833,8 +833,10 @@ struct BwdParams {
   int nsplit;             // shot parts: part h loops over shots [h S / nsplit, (h+1) S / nsplit)
   long long acc_copy;     // floats between the per-part accumulator copies (single writer per copy and launch)
   const float* W2;
-  const float* s_lvl;     // s^j for batch shot 0
+  const float* s_lvl;     // s^j for batch shot 0 (two-step kernel / reference of the plane indices below)
   long long s_shot_stride;
+  long long sj_plane0;    // plane of s^j for batch shot 0 in the s-tensor map (interior planes [nz][PI])
+  int sj_shot_planes;     // planes between consecutive shots' s^j
   float* acc;             // [nacc][Nz][P], index by slot (summed over shots and batches)
   const float* rho_res;   // slot 0 injection data [S][nt][nrec] (gradient), or null
   const float* rho_born;  // slot k >= 1 injection data [S][K][nt][nrec]
@@ -847,7 +849,7 @@ struct BwdParams {
 };
 
 template <bool SP>
-__device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMap* mt, const BwdParams& p,
+__device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMap* mt, const CUtensorMap* msj, const BwdParams& p,
                                          float* stages, uint64_t* bars) {
   const Geo& g = p.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
@@ -863,11 +865,15 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   int ps = sb, pt = 0, issued = 0;
   Ring prod;
   auto issue_next = [&]() {
-    float* st = stages + prod.stage * STAGE_FLOATS;
+    float* st = stages + prod.stage * BSTAGE_FLOATS;
     const int pl = (ps * p.nslot + p.slot0 + fb + pt) * p.nlev;
-    mbar_expect_tx(&bars[prod.stage], TILE_BYTES + (p.update ? PT_BYTES : 0));
+    const bool with_sj = p.imaging && pt == 0;  // s^j of the shot travels with its first field's stage
+    mbar_expect_tx(&bars[prod.stage], TILE_BYTES + (p.update ? PT_BYTES : 0) + (with_sj ? PT_BYTES : 0));
     tma_load_3d(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_in);
     if (p.update) tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_out);
+    if (with_sj)  // interior store: padded (x0, z0) is interior (x0 - c0, z0 - W); outside -> TMA zero fill
+      tma_load_3d(st + TILE_FLOATS + PT_FLOATS, msj, &bars[prod.stage], x0 - g.c0, z0 - g.W,
+                  static_cast<int>(p.sj_plane0 + static_cast<long long>(ps) * p.sj_shot_planes));
     prod.advance();
     if (++pt == nf) {
       pt = 0;
@@ -903,17 +909,6 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
     any_img |= img_rows[r];
     row_ok[r] = !SP || I < g.Nz;
   }
-  // imaging factor s^j of shot s for this thread's points (prefetched one shot ahead)
-  auto load_sj = [&](int s, float4 (&dst)[RZ]) {
-#pragma unroll
-    for (int r = 0; r < RZ; ++r) {
-      dst[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (img_rows[r])
-        dst[r] = ldg4(p.s_lvl + s * p.s_shot_stride + static_cast<long long>(I0 + r - g.W) * g.PI + jc);
-    }
-  };
-  float4 snext[RZ];
-  load_sj(sb, snext);
   BwdDamp<SP> dmp;
   dmp.init(g, I0, J0);
   const int tile_id = blockIdx.y * g.ntx + blockIdx.x;
@@ -937,23 +932,21 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
 
   Ring cons;
   for (int s = sb; s < se; ++s) {
-    float sj[RZ][4];
-#pragma unroll
-    for (int r = 0; r < RZ; ++r) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int ix = J0 + i - g.W;
-        sj[r][i] = (!SP || (ix >= 0 && ix < g.nx)) ? f4(snext[r], i) : 0.0f;
-      }
-    }
-    if (any_img && s + 1 < se) load_sj(s + 1, snext);
+    float sj[RZ][4];  // s^j of shot s at this thread's points, read from the first field's stage
     float* out_base = p.pool + (static_cast<long long>(s * p.nslot + p.slot0 + fb) * p.nlev + par_out) * g.plane;
 #pragma unroll
     for (int t = 0; t < BWD_FG; ++t) {
       if (t >= nf) break;
-      const float* st = stages + cons.stage * STAGE_FLOATS;
+      const float* st = stages + cons.stage * BSTAGE_FLOATS;
       float* dst = out_base + static_cast<long long>(t) * p.nlev * g.plane;
       mbar_wait(&bars[cons.stage], cons.phase);
+      if (t == 0) {
+#pragma unroll
+        for (int r = 0; r < RZ; ++r) {
+          const float4 v = p.imaging ? ld4(st + TILE_FLOATS + PT_FLOATS + so + r * TX) : make_float4(0.f, 0.f, 0.f, 0.f);
+          sj[r][0] = v.x, sj[r][1] = v.y, sj[r][2] = v.z, sj[r][3] = v.w;
+        }
+      }
 #if HV_BWD_PAIRED
       float2 L2[RZ][2], C2[RZ][2];
       lap_points(st, tx, ty, L2, C2);
@@ -1055,21 +1048,22 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
 
 __global__ void __launch_bounds__(NTHREADS, HV_BWD_MINB)
     bwd_step_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
-                    const BwdParams p) {
+                    const __grid_constant__ CUtensorMap msj, const BwdParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stages = reinterpret_cast<float*>(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + BSTAGES_BYTES);
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     tma_prefetch_desc(&mh);
     tma_prefetch_desc(&mt);
+    tma_prefetch_desc(&msj);
     for (int i = 0; i < NSTAGE; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (tile_is_interior(p.g, blockIdx.x * TX, blockIdx.y * TZ))
-    bwd_body<false>(&mh, &mt, p, stages, bars);
+    bwd_body<false>(&mh, &mt, &msj, p, stages, bars);
   else
-    bwd_body<true>(&mh, &mt, p, stages, bars);
+    bwd_body<true>(&mh, &mt, &msj, p, stages, bars);
 }
 
 // ------------------------------------------------------------------------------------------------ reverse (a6)

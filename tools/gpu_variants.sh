@@ -1,3 +1,4 @@
-# evidence lines with the resident-q forward (dev tool)
-timeout 900 python bench.py --config 4 --shots 4 --nt 400 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/bench_cfg4q.json 2>/dev/null; tail -1 gpurun_out/bench_cfg4q.json
-timeout 1200 python bench.py --config 3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/bench_cfg3q.json 2>/dev/null; tail -1 gpurun_out/bench_cfg3q.json
+# s^j through TMA in the backward (dev tool)
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q 2>&1 | tail -2
+for st in full checkpoint boundary; do echo "== $st"; python tools/tune.py --config 1 --S 16 --FG 0 --store $st --reps 2 2>&1 | tail -1; done
+echo "== 2 shots"; python tools/tune.py --config 1 --shots 2 --S 16 --FG 0 --reps 2 2>&1 | tail -1

@@ -303,6 +303,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   if ((st = make_tmap(c, pool, planes_per_shot * S, HX, HZ, &map_halo))) return st;
   if ((st = make_tmap(c, pool, planes_per_shot * S, TX, TZ, &map_tile))) return st;
   if ((st = make_tmap(c, Q ? Q : pool, Q ? K : planes_per_shot * S, TX, TZ, &map_q))) return st;
+  CUtensorMap map_w;
+  if ((st = make_tmap(c, W2, 1, TX, TZ, &map_w))) return st;
   // s^j tensor map of the backward (FULL store / BOUNDARY level buffer / CHECKPOINT segment)
   CUtensorMap map_sj = map_tile;
   if (adjoint) {
@@ -457,7 +459,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
         if (qres)
           fwd_qres_kernel<<<dim3(g.ntx, g.ntz, Gq), block, qres_smem, c->stream>>>(map_halo, map_tile, map_q, fp);
         else
-          fwd_step_kernel<<<gridf, block, fwd_smem, c->stream>>>(map_halo, map_tile, map_q, fp);
+          fwd_step_kernel<<<gridf, block, fwd_smem, c->stream>>>(map_halo, map_tile, map_q, map_w, fp);
         launches++;
       }
     }
@@ -602,7 +604,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
               for (int n = b; n < e; ++n) {
                 rp.n = n;
                 rp.s_out = seg + (size_t)(n - b) * g.iplane;
-                fwd_step_kernel<<<gridr, block, fwd_smem_bytes(0), c->stream>>>(map_halo, map_tile, map_q, rp);
+                fwd_step_kernel<<<gridr, block, fwd_smem_bytes(0), c->stream>>>(map_halo, map_tile, map_q, map_w, rp);
                 launches++;
               }
               cur_b = b;

@@ -353,7 +353,7 @@ __device__ __forceinline__ void fwd_unit_decode(const FwdParams& p, int u, int n
 __device__ __forceinline__ int group_begin(int K, int G, int grp) { return (K * grp) / G; }
 
 struct FwdProducer {  // thread 0's walk over this CTA's items (decoded once per unit: no divisions per item)
-  const CUtensorMap *mh, *mt, *mq;
+  const CUtensorMap *mh, *mt, *mq, *mw;
   float* stages;
   uint64_t* bars;
   int u, t;                 // current unit, next item within it (0 = background, 1..nf = Born fields)
@@ -389,9 +389,10 @@ struct FwdProducer {  // thread 0's walk over this CTA's items (decoded once per
     const int par_n = p.n & 1, par_new = par_n ^ 1;
     float* st = stages + ring.stage * FSTAGE_FLOATS;
     uint64_t* bar = &bars[ring.stage];
-    if (t == 0) {
-      mbar_expect_tx(bar, TILE_BYTES + (upd ? PT_BYTES : 0));
+    if (t == 0) {  // background: halo u^n, (leader) tile u^{n-1}, and the unit's w = dt^2 v^2 / h^2 tile
+      mbar_expect_tx(bar, TILE_BYTES + (upd ? PT_BYTES : 0) + PT_BYTES);
       tma_load_3d(st, mh, bar, x0 - R, z0 - R, pl_bg + par_n);
+      tma_load_3d(st + TILE_FLOATS + PT_FLOATS, mw, bar, x0, z0, 0);
 #if HV_L2_HINTS
       if (upd) tma_load_3d_hint(st + TILE_FLOATS, mt, bar, x0, z0, pl_bg + par_new, pol_first);
 #else
@@ -433,12 +434,7 @@ __device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages
   const int J0 = x0 + tx * 4;
   const int so = ty * RZ * TX + tx * 4;                       // smem offset of this thread's first point
   const long long go = static_cast<long long>(I0) * g.P + J0;  // plane offset of this thread's first point
-  float2 w[RZ][2];
-#pragma unroll
-  for (int r = 0; r < RZ; ++r) {
-    const float4 wv = ldg4(p.W2 + static_cast<long long>(min(I0 + r, g.Nz - 1)) * g.P + J0);
-    w[r][0] = lo2(wv), w[r][1] = hi2(wv);
-  }
+  float2 w[RZ][2];  // from the background item's stage (TMA), below
   bool row_ok[RZ];
 #pragma unroll
   for (int r = 0; r < RZ; ++r) row_ok[r] = !SP || I0 + r < g.Nz;
@@ -484,6 +480,11 @@ __device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages
   {
     const float* st = stages + cons.stage * FSTAGE_FLOATS;
     mbar_wait(&bars[cons.stage], cons.phase);
+#pragma unroll
+    for (int r = 0; r < RZ; ++r) {
+      const float4 wv = ld4(st + TILE_FLOATS + PT_FLOATS + so + r * TX);
+      w[r][0] = lo2(wv), w[r][1] = hi2(wv);
+    }
     float2 C[RZ][2];
     lap_points(st, tx, ty, Lb, C);
     if (leader) {
@@ -573,7 +574,8 @@ __device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages
 #endif
 __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
     fwd_step_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
-                    const __grid_constant__ CUtensorMap mq, const FwdParams p) {
+                    const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mw,
+                    const FwdParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stages = reinterpret_cast<float*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + FSTAGES_BYTES);
@@ -590,7 +592,7 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
   const int U = p.S * p.G * ntl;
   const int nstep = gridDim.x;
   FwdProducer prod;
-  prod.mh = &mh, prod.mt = &mt, prod.mq = &mq, prod.stages = stages, prod.bars = bars;
+  prod.mh = &mh, prod.mt = &mt, prod.mq = &mq, prod.mw = &mw, prod.stages = stages, prod.bars = bars;
   prod.u = blockIdx.x, prod.t = 0, prod.U = U, prod.nstep = nstep, prod.ntl = ntl;
   prod.pol_first = policy_evict_first(), prod.pol_last = policy_evict_last();
   prod.decode(p);

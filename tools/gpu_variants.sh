@@ -1,5 +1,4 @@
-# backward stages 4 vs 3 with the s^j stage (dev tool)
-for i in 1 2; do
-echo "== ns3"; python tools/tune.py --config 1 --S 16 --FG 0 --reps 2 2>&1 | tail -1
-echo "== ns4"; HV_LIB=build/libhv_ns4.so python tools/tune.py --config 1 --S 16 --FG 0 --reps 2 2>&1 | tail -1
-done
+# forward w tile through TMA (dev tool)
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q 2>&1 | tail -2
+for i in 1 2; do python tools/tune.py --config 1 --S 16 --FG 0 --reps 2 2>&1 | tail -1; done
+python tools/tune.py --config 1 --shots 2 --S 16 --FG 0 --reps 2 2>&1 | tail -1

@@ -1,4 +1,5 @@
-# forward w tile through TMA (dev tool)
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q 2>&1 | tail -2
-for i in 1 2; do python tools/tune.py --config 1 --S 16 --FG 0 --reps 2 2>&1 | tail -1; done
-python tools/tune.py --config 1 --shots 2 --S 16 --FG 0 --reps 2 2>&1 | tail -1
+# ncu evidence on the cfg 4 grid: resident-q forward and backward (dev tool)
+P="python tools/profile_step.py --config 4 --shots 4 --nt 60 --reps 1"
+$P > /dev/null 2>&1; echo plain=$?
+ncu --set full --clock-control none -k regex:fwd_qres -s 20 -c 1 -o gpurun_out/prof_qres_cfg4 $P > gpurun_out/ncu_qres.log 2>&1; echo q=$?
+ncu --set full --clock-control none -k regex:bwd_step -s 20 -c 1 -o gpurun_out/prof_bwd_cfg4 $P > gpurun_out/ncu_bwd4.log 2>&1; echo b=$?

@@ -15,11 +15,14 @@ ap.add_argument("--S", type=int, default=0)
 ap.add_argument("--FG", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--shots", type=int, default=0)
+ap.add_argument("--nt", type=int, default=0)
 ap.add_argument("--store", default="auto")
 a = ap.parse_args()
 wl = W.config(a.config)
 if a.shots:
     wl = wl.subset(shots=range(a.shots))
+if a.nt:
+    wl = wl.subset(nt=a.nt)
 V = torch.from_numpy(wl.probes()).cuda()
 m = torch.from_numpy(wl.model).cuda()
 s = hv.Solver.from_workload(wl, shot_batch=a.S, field_group=a.FG, store=a.store)

@@ -98,7 +98,9 @@ HV_API int hv_forward(hv_ctx* ctx, const float* m, float* d);
 HV_API int hv_gradient(hv_ctx* ctx, const float* m, const float* d_obs, float* g, double* phi);
 
 /* Gauss-Newton H_d [v_1..v_K] over the shard: V, HV [K][nz][nx]. K >= 1. All K probes of a shot share one
- * background wavefield (batched probing). */
+ * background wavefield (batched probing). Bit-deterministic for a given shard and shot
+ * batching (every accumulator address has one writer per launch; launches are ordered), and row k does not
+ * depend on the other probes of the batch. */
 HV_API int hv_hessvec(hv_ctx* ctx, const float* m, int32_t K, const float* V, float* HV);
 
 /* Fused: gradient and K Hessian-vector products in one pass over the shard (1 + K fields forward,

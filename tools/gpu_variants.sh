@@ -1,5 +1,3 @@
-# ncu evidence on the cfg 4 grid: resident-q forward and backward (dev tool)
-P="python tools/profile_step.py --config 4 --shots 4 --nt 60 --reps 1"
-$P > /dev/null 2>&1; echo plain=$?
-ncu --set full --clock-control none -k regex:fwd_qres -s 20 -c 1 -o gpurun_out/prof_qres_cfg4 $P > gpurun_out/ncu_qres.log 2>&1; echo q=$?
-ncu --set full --clock-control none -k regex:bwd_step -s 20 -c 1 -o gpurun_out/prof_bwd_cfg4 $P > gpurun_out/ncu_bwd4.log 2>&1; echo b=$?
+# resident-q vs one-wave forward on cfg 2 (Q = 16 MB) (dev tool)
+for q in 0 1; do echo "== cfg2 qres $q"; HV_QRES=$q python tools/tune.py --config 2 --shots 22 --S 22 --FG 0 --reps 1 2>&1 | tail -1; done
+for q in 0 1; do echo "== cfg2 qres $q qfg 8"; HV_QRES=$q HV_QFG=8 python tools/tune.py --config 2 --shots 22 --S 22 --FG 0 --reps 1 2>&1 | tail -1; done

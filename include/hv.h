@@ -23,8 +23,13 @@
  *         never accumulated into.
  * Calls are blocking (they return when the result is complete) and are serialised per context; use one context
  * per GPU. No call falls back to the CPU: without a usable sm_100a device hv_create fails with HV_ECUDA.
- * Multi-GPU: each rank passes its shot shard [src_begin, src_end); gradient / hessvec return RANK-LOCAL partial
- * sums over that shard (the per-source terms of PAPER.md:164); the caller all-reduces them (NCCL).
+ * Multi-GPU: each rank passes its shot shard [src_begin, src_end) (may be empty); gradient / hessvec / misfit
+ * return RANK-LOCAL partial sums over that shard (the per-source terms of PAPER.md:164) unless a NCCL communicator
+ * is attached (hv_config.nccl_comm / hv_set_comm): then the library all-reduces g, H.v and phi in-library on its
+ * stream before returning, and every rank receives the sum over all shots.
+ * Streams: with no stream bound (hv_set_stream NULL) a call first waits for the work already queued on the legacy
+ * default stream (e.g. torch's default stream), so device inputs produced there are complete; with a bound stream
+ * the call is ordered on that stream.
  */
 #ifndef HV_H
 #define HV_H
@@ -50,6 +55,7 @@ extern "C" {
 #define HV_ENOMEM  4  /* the plan exceeds the device-memory budget                                        */
 #define HV_ECUDA   5  /* CUDA / cuFFT error, or no sm_100 device                                          */
 #define HV_ESTATE  6  /* null / destroyed context                                                         */
+#define HV_ENCCL   7  /* NCCL unavailable (libnccl.so.2 not loadable) or an NCCL call failed              */
 
 /* forward-history storage for the reverse pass (not in the paper) */
 #define HV_STORE_AUTO       0  /* FULL when it fits the budget, else CHECKPOINT                      */
@@ -81,20 +87,37 @@ typedef struct {
   int32_t device;        /* CUDA device ordinal                                                          */
   size_t  mem_budget;    /* bytes of device memory the plan may use; 0 = 90 % of (free memory + the
                             context's own H.v workspace, which a larger plan releases and re-allocates)   */
+  void   *nccl_comm;     /* optional ncclComm_t (NULL: rank-local partial sums). Borrowed, not owned: it must
+                            outlive the context's calls. One rank per GPU; every rank must make the same
+                            sequence of gradient / hessvec / misfit calls (the all-reduces are collective).   */
 } hv_config;
 
-/* Create / destroy. Validates geometry (indices inside the interior grid) -> HV_EINVAL. */
+/* Create / destroy. Validates geometry (indices inside the interior grid) -> HV_EINVAL. An empty shard
+ * (src_begin == src_end, e.g. more ranks than shots) is allowed: its partial sums are zero. */
 HV_API int hv_create(const hv_config* cfg, hv_ctx** out);
 HV_API int hv_destroy(hv_ctx* ctx);
 
 /* Run subsequent work on this cudaStream_t (NULL = the context's own stream). */
 HV_API int hv_set_stream(hv_ctx* ctx, void* cuda_stream);
 
+/* Attach (or detach with NULL) a NCCL communicator for in-library reductions (see hv_config.nccl_comm). */
+HV_API int hv_set_comm(hv_ctx* ctx, void* nccl_comm);
+
 /* d = f(m) for the shard's shots: m [nz][nx] (m/s); d [src_end - src_begin][nt][nrec]; d[:,0,:] = 0. */
 HV_API int hv_forward(hv_ctx* ctx, const float* m, float* d);
 
+/* d = f(m) for ONE shot ("given a source location x_s ... solve the wave equation"): isrc is the
+ * GLOBAL shot index, src_begin <= isrc < src_end (else HV_EINVAL); d [nt][nrec]. */
+HV_API int hv_forward_shot(hv_ctx* ctx, const float* m, int32_t isrc, float* d);
+
+/* Data misfit only, Phi_d(m) = 1/2 sum_s sum_{n,r} (f_s(m) - d_obs,s)^2 (the likelihood term of Phi, PAPER.md:104-106;
+ * what each gpCN proposal evaluates): forward sweeps + residual, no history store, no adjoint.
+ * d_obs [local shots][nt][nrec]; *phi float64, summed in a fixed order (bit-deterministic). */
+HV_API int hv_misfit(hv_ctx* ctx, const float* m, const float* d_obs, double* phi);
+
 /* Misfit gradient and value over the shard: d_obs [local shots][nt][nrec]; g [nz][nx];
- * *phi = 1/2 sum (d - d_obs)^2 accumulated in float64 (phi may be NULL). */
+ * *phi = 1/2 sum (d - d_obs)^2 accumulated in float64 in a fixed order (phi may be NULL). g and phi are
+ * bit-deterministic for a given shard and shot batching. */
 HV_API int hv_gradient(hv_ctx* ctx, const float* m, const float* d_obs, float* g, double* phi);
 
 /* Gauss-Newton H_d [v_1..v_K] over the shard: V, HV [K][nz][nx]. K >= 1. All K probes of a shot share one
@@ -175,6 +198,14 @@ HV_API int hv_lowrank_geneig(hv_ctx* ctx, const float* m, int32_t r, int32_t K, 
 HV_API int hv_psf_plus(hv_ctx* ctx, int32_t nz, int32_t nx, int32_t nr, const float* rows, const float* w, int32_t nc,
                        const float* cols, const int32_t* col_kz, const int32_t* col_kx, int32_t rank, float* A,
                        float* B, double* alpha);
+
+/* ---- NCCL helpers (the library dlopens libnccl.so.2; nothing links against it). Rank 0 calls hv_nccl_unique_id
+ * and shares the 128 bytes with the other ranks (e.g. a torch.distributed broadcast); every rank then calls
+ * hv_nccl_comm_create with its rank and CUDA device. The caller owns the communicator (hv_nccl_comm_destroy). */
+HV_API int hv_nccl_unique_id(void* id_out /* 128 bytes */);
+HV_API int hv_nccl_comm_create(int32_t nranks, int32_t rank, const void* id /* 128 bytes */, int32_t device,
+                               void** comm_out);
+HV_API int hv_nccl_comm_destroy(void* comm);
 
 /* Counters of the last call (for benches). */
 typedef struct {

@@ -8,7 +8,9 @@ sm_100 device raises `HVError` (status HV_ECUDA).
 
 Arrays may be numpy arrays (host; the library copies them in/out inside the call, which is
 what the end-to-end bench measures) or torch CUDA tensors (device; zero-copy, work ordered on
-torch's current stream). Layout: [nz][nx] float32 row-major; data [shot][nt][nrec]; probes [K][nz][nx].
+torch's current stream: a non-default stream is bound with hv_set_stream, and on torch's default
+stream the library's own stream first waits for the legacy default stream). Layout: [nz][nx]
+float32 row-major; data [shot][nt][nrec]; probes [K][nz][nx].
 """
 from __future__ import annotations
 
@@ -23,8 +25,9 @@ __all__ = ["Solver", "HVError", "lib", "STORE", "psido_apply"]
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HV_LIB") or os.path.join(_HERE, "libhv.so")  # HV_LIB: tuning variants only
 
-HV_OK, HV_EINVAL, HV_EGRID, HV_ECFL, HV_ENOMEM, HV_ECUDA, HV_ESTATE = range(7)
-STATUS = {0: "HV_OK", 1: "HV_EINVAL", 2: "HV_EGRID", 3: "HV_ECFL", 4: "HV_ENOMEM", 5: "HV_ECUDA", 6: "HV_ESTATE"}
+HV_OK, HV_EINVAL, HV_EGRID, HV_ECFL, HV_ENOMEM, HV_ECUDA, HV_ESTATE, HV_ENCCL = range(8)
+STATUS = {0: "HV_OK", 1: "HV_EINVAL", 2: "HV_EGRID", 3: "HV_ECFL", 4: "HV_ENOMEM", 5: "HV_ECUDA", 6: "HV_ESTATE",
+          7: "HV_ENCCL"}
 STORE = {"auto": 0, "full": 1, "checkpoint": 2, "boundary": 3}
 
 
@@ -46,7 +49,7 @@ class HvConfig(ctypes.Structure):
         ("src_begin", ctypes.c_int32), ("src_end", ctypes.c_int32),
         ("store", ctypes.c_int32), ("ckpt_interval", ctypes.c_int32),
         ("shot_batch", ctypes.c_int32), ("field_group", ctypes.c_int32),
-        ("device", ctypes.c_int32), ("mem_budget", ctypes.c_size_t),
+        ("device", ctypes.c_int32), ("mem_budget", ctypes.c_size_t), ("nccl_comm", ctypes.c_void_p),
     ]
 
 
@@ -75,6 +78,12 @@ def lib() -> ctypes.CDLL:
         L.hv_destroy.argtypes = [vp]
         L.hv_set_stream.argtypes = [vp, vp]
         L.hv_forward.argtypes = [vp, fp, fp]
+        L.hv_forward_shot.argtypes = [vp, fp, i32, fp]
+        L.hv_misfit.argtypes = [vp, fp, fp, ctypes.POINTER(ctypes.c_double)]
+        L.hv_set_comm.argtypes = [vp, vp]
+        L.hv_nccl_unique_id.argtypes = [vp]
+        L.hv_nccl_comm_create.argtypes = [i32, i32, vp, i32, ctypes.POINTER(ctypes.c_void_p)]
+        L.hv_nccl_comm_destroy.argtypes = [vp]
         L.hv_gradient.argtypes = [vp, fp, fp, fp, ctypes.POINTER(ctypes.c_double)]
         L.hv_hessvec.argtypes = [vp, fp, i32, fp, fp]
         L.hv_gradient_hessvec.argtypes = [vp, fp, fp, i32, fp, fp, ctypes.POINTER(ctypes.c_double), fp]
@@ -90,7 +99,9 @@ def lib() -> ctypes.CDLL:
         L.hv_get_stats.argtypes = [vp, ctypes.POINTER(HvStats)]
         L.hv_last_error.argtypes = [vp]
         L.hv_last_error.restype = ctypes.c_char_p
-        for name in ("hv_create", "hv_destroy", "hv_set_stream", "hv_forward", "hv_gradient", "hv_hessvec",
+        for name in ("hv_create", "hv_destroy", "hv_set_stream", "hv_forward", "hv_forward_shot", "hv_misfit",
+                     "hv_set_comm", "hv_nccl_unique_id", "hv_nccl_comm_create", "hv_nccl_comm_destroy",
+                     "hv_gradient", "hv_hessvec",
                      "hv_gradient_hessvec", "hv_psido_apply", "hv_get_stats", "hv_psf_rows", "hv_psf_weights",
                      "hv_pdo_columns", "hv_pdo_weights", "hv_highpass", "hv_lowrank_geneig", "hv_psf_plus"):
             getattr(L, name).restype = ctypes.c_int
@@ -136,7 +147,8 @@ class Solver:
     def __init__(self, *, nz: int, nx: int, h: float, dt: float, nt: int, sponge: int, v_ref: float,
                  src: np.ndarray, rec: np.ndarray, wavelet: np.ndarray, src_begin: int = 0,
                  src_end: Optional[int] = None, store: str = "auto", ckpt_interval: int = 0,
-                 shot_batch: int = 0, field_group: int = 0, device: int = 0, mem_budget: int = 0):
+                 shot_batch: int = 0, field_group: int = 0, device: int = 0, mem_budget: int = 0,
+                 nccl_comm: Optional[int] = None):
         L = lib()
         self._src = np.ascontiguousarray(src, dtype=np.int32)
         self._rec = np.ascontiguousarray(rec, dtype=np.int32)
@@ -151,7 +163,8 @@ class Solver:
             wavelet=self._wav.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
             src_begin=src_begin, src_end=(len(self._src) if src_end is None else src_end),
             store=STORE[store] if isinstance(store, str) else int(store), ckpt_interval=ckpt_interval,
-            shot_batch=shot_batch, field_group=field_group, device=device, mem_budget=mem_budget)
+            shot_batch=shot_batch, field_group=field_group, device=device, mem_budget=mem_budget,
+            nccl_comm=nccl_comm)
         h_ = ctypes.c_void_p()
         st = L.hv_create(ctypes.byref(cfg), ctypes.byref(h_))
         if st != HV_OK:
@@ -200,6 +213,30 @@ class Solver:
         self._stream(a, o)
         self._check(lib().hv_forward(self._h, a.ptr, o.ptr))
         return o.obj
+
+    def forward_shot(self, m, isrc: int, out=None):
+        """d = f(m) for ONE shot, global index isrc in [src_begin, src_end): [nt][nrec]."""
+        a = _Arr(m, shape=(self.nz, self.nx), name="m")
+        shape = (self.nt, self.nrec)
+        o = _Arr(out if out is not None else _empty_like_kind(a, shape), shape=shape, name="d")
+        self._stream(a, o)
+        self._check(lib().hv_forward_shot(self._h, a.ptr, int(isrc), o.ptr))
+        return o.obj
+
+    def misfit(self, m, d_obs) -> float:
+        """Phi_d(m) = 1/2 sum (f(m) - d_obs)^2 over the shard: forward + residual only, no adjoint (the
+        likelihood each gpCN proposal evaluates)."""
+        a = _Arr(m, shape=(self.nz, self.nx), name="m")
+        d = _Arr(d_obs, shape=(self.nloc, self.nt, self.nrec), name="d_obs")
+        phi = ctypes.c_double(0.0)
+        self._stream(a, d)
+        self._check(lib().hv_misfit(self._h, a.ptr, d.ptr, ctypes.byref(phi)))
+        return phi.value
+
+    def set_comm(self, comm: Optional[int]):
+        """Attach a NCCL communicator (from `nccl_comm_create`): g, H·v and phi are then summed over the ranks
+        in-library. None detaches it (rank-local partial sums)."""
+        self._check(lib().hv_set_comm(self._h, ctypes.c_void_p(comm) if comm else None))
 
     def gradient(self, m, d_obs, out=None):
         """(phi, g): misfit and its gradient F*(f(m) - d_obs) over the shard."""
@@ -360,3 +397,31 @@ class Solver:
 
 def psido_apply(solver: Solver, a, b, v, mode: int = 0):
     return solver.psido_apply(a, b, v, mode)
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; share it with the other ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    st = lib().hv_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p))
+    if st != HV_OK:
+        raise HVError(st, "hv_nccl_unique_id failed")
+    return buf.raw
+
+
+def nccl_comm_create(nranks: int, rank: int, uid: bytes, device: int) -> int:
+    """A NCCL communicator for the library's in-library reductions (caller owns it: nccl_comm_destroy)."""
+    if len(uid) != 128:
+        raise ValueError("uid must be 128 bytes")
+    buf = ctypes.create_string_buffer(uid, 128)
+    out = ctypes.c_void_p()
+    st = lib().hv_nccl_comm_create(int(nranks), int(rank), ctypes.cast(buf, ctypes.c_void_p), int(device),
+                                   ctypes.byref(out))
+    if st != HV_OK:
+        raise HVError(st, "hv_nccl_comm_create failed")
+    return int(out.value)
+
+
+def nccl_comm_destroy(comm: int) -> None:
+    st = lib().hv_nccl_comm_destroy(ctypes.c_void_p(comm))
+    if st != HV_OK:
+        raise HVError(st, "hv_nccl_comm_destroy failed")

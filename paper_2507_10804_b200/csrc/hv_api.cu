@@ -48,6 +48,7 @@ int make_tmap(hv_ctx* c, const float* base, long long nplanes, int box_w, int bo
 }
 
 constexpr bool kTwoStepDefault = false;
+constexpr int kPhiBlocks = 1024;  // residual kernel grid: fixed, so phi's summation order never changes
 constexpr int kQresFG = 6;  // resident-q forward: Born fields per CTA (6 q_k tiles + 3 stages: 2 CTAs per SM)
 // Backward CTAs per (tile, field group): the batch's shots are split into this many parts, each summing its
 // imaging terms into its own accumulator copy (finalize adds the copies in a fixed order). 2 halves the last
@@ -77,7 +78,20 @@ int grid1d(long long n) { return static_cast<int>(std::min<long long>((n + 255) 
 
 // ------------------------------------------------------------------------------------------ the plan
 
-enum Want { W_FORWARD = 1, W_GRAD = 2, W_HESS = 4 };
+enum Want { W_FORWARD = 1, W_GRAD = 2, W_HESS = 4, W_MISFIT = 8 };
+
+// CUDA events of one call, destroyed on every return path.
+struct Events {
+  std::vector<cudaEvent_t> v;
+  ~Events() {
+    for (cudaEvent_t e : v) cudaEventDestroy(e);
+  }
+  cudaError_t make(cudaEvent_t* e) {
+    const cudaError_t r = cudaEventCreate(e);
+    if (r == cudaSuccess) v.push_back(*e);
+    return r;
+  }
+};
 
 struct Plan {
   int store = HV_STORE_FULL;
@@ -91,10 +105,10 @@ struct Plan {
   double per_shot = 0; // bytes
 };
 
-int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
+int plan_call(hv_ctx* c, int want, int K, int nloc, Plan* pl) {
   const Geo& g = c->g;
   const double F4 = 4.0;
-  const bool grad = want & W_GRAD;
+  const bool grad = want & (W_GRAD | W_MISFIT);  // background data + residual per shot
   const bool adjoint = want & (W_GRAD | W_HESS);
   pl->nslot = 1 + K + (adjoint ? 1 : 0);  // + replay slot (CHECKPOINT)
   pl->nacc = adjoint ? 1 + K : 0;
@@ -106,7 +120,7 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
   // the context's own workspace (grow-only, reused or re-allocated by this call) counts as available
   // (only the buffers of the H·v path: callers such as hv_lowrank_geneig hold their own across hv_hessvec calls)
   static const char* const kPathBufs[] = {"W2",   "imgc", "rec_coef", "scalars", "Q",    "pool", "dborn", "dbg",
-                                          "rres", "acc",  "store",    "ring",    "sbuf", "ckpt", "seg"};
+                                          "rres", "acc",  "store",    "ring",    "sbuf", "ckpt", "seg", "phi_part"};
   double held = 0;
   for (const char* n : kPathBufs) {
     auto it = c->ws.find(n);
@@ -153,10 +167,10 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
   const int ntiles = g.ntx * g.ntz;
   if (S <= 0) S = 32;  // every CTA loops over the batch's shots: more shots amortise q_k loads and imaging writes
   S = std::min(S, fit);
-  S = std::max(1, std::min(S, c->nloc));
-  if (c->cfg.shot_batch <= 0) {  // equal batches: ceil(nloc / S) batches of near-equal size (no 1-shot tail)
-    const int nb = (c->nloc + S - 1) / S;
-    S = (c->nloc + nb - 1) / nb;
+  S = std::max(1, std::min(S, nloc));
+  if (c->cfg.shot_batch <= 0 && nloc > 0) {  // equal batches: ceil(nloc / S) of near-equal size (no 1-shot tail)
+    const int nb = (nloc + S - 1) / S;
+    S = (nloc + nb - 1) / nb;
   }
   pl->S = S;
   // forward Born fields per unit (groups are near-equal): fewer groups = fewer background recomputes per shot and
@@ -200,14 +214,17 @@ int plan_call(hv_ctx* c, int want, int K, Plan* pl) {
 
 // ------------------------------------------------------------------------------------------ one call
 
+// One call over the shard-local shots [lo, hi) (hi < 0: the whole shard). want: W_FORWARD (d), W_MISFIT (phi
+// only), W_GRAD (phi, g), W_HESS (HV); W_GRAD | W_HESS is the fused pass.
 int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, const float* V_in, float* d_user,
-        float* g_user, double* phi_user, float* hv_user) {
+        float* g_user, double* phi_user, float* hv_user, int lo = 0, int hi = -1) {
   if (!c) return HV_ESTATE;
   c->err.clear();
-  CU_TRY(cudaSetDevice(c->dev));
+  if (const int e_ = hvrt::enter(c)) return e_;
   const Geo& g = c->g;
-  const int nloc = c->nloc;
-  const bool grad = want & W_GRAD, hess = want & W_HESS, fwd = want & W_FORWARD;
+  if (hi < 0) hi = c->nloc;
+  const int nloc = hi - lo;  // shots of this call
+  const bool grad = want & W_GRAD, hess = want & W_HESS, fwd = want & W_FORWARD, misfit = want & W_MISFIT;
   if (hess && K < 1 && !grad) return fail(c, HV_EINVAL, "K must be >= 1");
   if (K < 0) return fail(c, HV_EINVAL, "K must be >= 0");
   c->launches = 0;
@@ -215,15 +232,16 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   const size_t mbytes = sizeof(float) * (size_t)g.nz * g.nx;
   const size_t dbytes = sizeof(float) * (size_t)nloc * g.nt * g.nrec;
 
+  Events evg;  // every event of this call; destroyed on all return paths
   cudaEvent_t ev0, ev1;
-  CU_TRY(cudaEventCreate(&ev0));
-  CU_TRY(cudaEventCreate(&ev1));
+  CU_TRY(evg.make(&ev0));
+  CU_TRY(evg.make(&ev1));
   CU_TRY(cudaEventRecord(ev0, c->stream));
 
   const float *m = nullptr, *dobs = nullptr, *V = nullptr;
   int st = stage_in(c, "in_m", m_in, mbytes, reinterpret_cast<const void**>(&m));
   if (st) return st;
-  if (grad) {
+  if ((grad || misfit) && dbytes > 0) {
     st = stage_in(c, "in_dobs", dobs_in, dbytes, reinterpret_cast<const void**>(&dobs));
     if (st) return st;
   }
@@ -232,12 +250,12 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     if (st) return st;
   }
   OutStage o_d, o_g, o_hv;
-  if (fwd && (st = stage_out(c, "out_d", d_user, dbytes, &o_d))) return st;
+  if (fwd && dbytes > 0 && (st = stage_out(c, "out_d", d_user, dbytes, &o_d))) return st;
   if (grad && (st = stage_out(c, "out_g", g_user, mbytes, &o_g))) return st;
   if (K > 0 && (st = stage_out(c, "out_hv", hv_user, mbytes * (size_t)K, &o_hv))) return st;
 
   Plan pl;
-  if ((st = plan_call(c, want, K, &pl))) return st;
+  if ((st = plan_call(c, want, K, nloc, &pl))) return st;
   const int S = pl.S;
   const bool adjoint = grad || K > 0;
   const int nslot = pl.nslot;
@@ -251,19 +269,25 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   if ((st = ws_get(c, "imgc", sizeof(float) * g.iplane, (void**)&imgc))) return st;
   if ((st = ws_get(c, "rec_coef", sizeof(float) * g.nrec, (void**)&rec_coef))) return st;
   if ((st = ws_get(c, "scalars", 64, (void**)&vmax))) return st;
+  unsigned int* vmin = vmax + 1;  // float bits read as int: any value <= 0 makes it <= 0
   phi_d = reinterpret_cast<double*>(reinterpret_cast<char*>(vmax) + 8);
   CU_TRY(cudaMemsetAsync(vmax, 0, 64, c->stream));
+  CU_TRY(cudaMemsetAsync(vmin, 0x7f, 4, c->stream));  // 0x7f7f7f7f = 3.4e38
   const float h = c->cfg.h, dt = c->cfg.dt;
   const float dt2_h2 = dt * dt / (h * h), two_dt2_h2 = 2.0f * dt * dt / (h * h);
-  model_setup_kernel<<<grid1d(g.plane), 256, 0, c->stream>>>(g, m, dt2_h2, two_dt2_h2, W2, imgc, vmax);
+  model_setup_kernel<<<grid1d(g.plane), 256, 0, c->stream>>>(g, m, dt2_h2, two_dt2_h2, W2, imgc, vmax,
+                                                               reinterpret_cast<int*>(vmin));
   rec_coef_kernel<<<(g.nrec + 255) / 256, 256, 0, c->stream>>>(g, m, c->d_recI, c->d_recJ, rec_coef);
   launches += 2;
-  unsigned int vbits = 0;
-  CU_TRY(cudaMemcpyAsync(&vbits, vmax, 4, cudaMemcpyDeviceToHost, c->stream));
+  unsigned int vbits[2] = {0, 0};
+  CU_TRY(cudaMemcpyAsync(vbits, vmax, 8, cudaMemcpyDeviceToHost, c->stream));
   CU_TRY(cudaStreamSynchronize(c->stream));
-  float vmx;
-  std::memcpy(&vmx, &vbits, 4);
-  if (!(vmx > 0.0f) || !std::isfinite(vmx)) return fail(c, HV_EINVAL, "model must be positive and finite");
+  float vmx, vmn;
+  std::memcpy(&vmx, &vbits[0], 4);
+  std::memcpy(&vmn, &vbits[1], 4);
+  if (!(vmx > 0.0f) || !std::isfinite(vmx) || !(vmn > 0.0f))
+    return fail(c, HV_EINVAL, "model must be positive and finite (min " + std::to_string(vmn) + ", max " +
+                                  std::to_string(vmx) + ")");
   if (dt * vmx / h > 0.5546f)
     return fail(c, HV_ECFL, "CFL: dt*max(m)/h = " + std::to_string(dt * vmx / h) + " > 0.5546");
 
@@ -282,9 +306,11 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   const bool use_t2 = pl.nlev == 4;
   if ((st = ws_get(c, "pool", sizeof(float) * g.plane * planes_per_shot * S, (void**)&pool))) return st;
   if (K > 0 && (st = ws_get(c, "dborn", sizeof(float) * (size_t)S * K * g.nt * g.nrec, (void**)&dborn))) return st;
-  if (grad) {
+  double* phi_part = nullptr;  // per-block partial sums of the residual kernel (fixed-order phi, no atomics)
+  if (grad || misfit) {
     if ((st = ws_get(c, "dbg", sizeof(float) * (size_t)S * g.nt * g.nrec, (void**)&dbg))) return st;
     if ((st = ws_get(c, "rres", sizeof(float) * (size_t)S * g.nt * g.nrec, (void**)&rres))) return st;
+    if ((st = ws_get(c, "phi_part", sizeof(double) * kPhiBlocks, (void**)&phi_part))) return st;
   }
   if (adjoint) {
     if ((st = ws_get(c, "acc", sizeof(float) * g.plane * pl.nacc * kBwdSplit, (void**)&acc))) return st;
@@ -313,7 +339,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     else st = make_tmap_interior(c, seg, (long long)S * pl.k, &map_sj);
     if (st) return st;
   }
-  if (phi_user) CU_TRY(cudaMemsetAsync(phi_d, 0, sizeof(double), c->stream));
+  CU_TRY(cudaMemsetAsync(phi_d, 0, sizeof(double), c->stream));
 
   // --- the shot batches
   const int FG = pl.FG;
@@ -341,7 +367,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   std::vector<cudaEvent_t> evs;
   int64_t graph_launches = 0;
   auto new_event = [&](cudaEvent_t* e) -> int {
-    CU_TRY(cudaEventCreate(e));
+    CU_TRY(evg.make(e));
     evs.push_back(*e);
     return HV_OK;
   };
@@ -381,8 +407,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     fp.d_born = dborn;
     if (fwd) {
       fp.d_bg = reinterpret_cast<float*>(o_d.dev);
-      fp.dbg_shot0 = b0;
-    } else if (grad) {
+      fp.dbg_shot0 = b0 - lo;
+    } else if (grad || misfit) {
       fp.d_bg = dbg;
       fp.dbg_shot0 = 0;
     }
@@ -477,13 +503,14 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     return HV_OK;
     }
     CU_TRY(cudaGetLastError());
+    if (grad || misfit) {  // K4: rho = d - d_obs; phi += 1/2 |rho|^2 in a fixed order (block partials, one reducer)
+      const long long nres = (long long)Sb * g.nt * g.nrec;
+      residual_kernel<<<kPhiBlocks, 256, 0, c->stream>>>(nres, dbg, dobs + (size_t)(b0 - lo) * g.nt * g.nrec, rres,
+                                                          phi_part);
+      phi_reduce_kernel<<<1, 32, 0, c->stream>>>(phi_part, kPhiBlocks, phi_d);
+      launches += 2;
+    }
     if (adjoint) {
-      if (grad) {
-        const long long nres = (long long)Sb * g.nt * g.nrec;
-        residual_kernel<<<grid1d(nres), 256, 0, c->stream>>>(nres, dbg, dobs + (size_t)b0 * g.nt * g.nrec, rres,
-                                                              phi_d);
-        launches++;
-      }
       if (boundary) {  // keep u^{nt-1}, u^{nt-2} (slot 0) in the replay slot; clear the adjoint slots
         for (int s = 0; s < Sb; ++s) {
           float* base = pool + (size_t)s * planes_per_shot * g.plane;
@@ -627,8 +654,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     return HV_OK;
   };
   const bool use_graphs = std::getenv("HV_NO_GRAPHS") == nullptr;
-  for (int b0 = 0; b0 < nloc; b0 += S) {
-    const int Sb = std::min(S, nloc - b0);
+  for (int b0 = lo; b0 < hi; b0 += S) {
+    const int Sb = std::min(S, hi - b0);
     cudaEvent_t ev4[4];
     for (int e = 0; e < 4; ++e)
       if ((st = new_event(&ev4[e]))) return st;
@@ -694,7 +721,13 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     launches++;
   }
   CU_TRY(cudaGetLastError());
-  if (fwd && (st = finish_out(c, o_d))) return st;
+  // a8 across GPUs: with a communicator attached, sum g / H·v / phi over the ranks in-library (NCCL on this stream)
+  if (c->nccl_comm && (grad || misfit || K > 0)) {
+    if (grad && (st = nccl_allreduce_sum(c, o_g.dev, (size_t)g.nz * g.nx, 0))) return st;
+    if (K > 0 && (st = nccl_allreduce_sum(c, o_hv.dev, (size_t)K * g.nz * g.nx, 0))) return st;
+    if ((st = nccl_allreduce_sum(c, phi_d, 1, 1))) return st;
+  }
+  if (fwd && dbytes > 0 && (st = finish_out(c, o_d))) return st;
   if (grad && (st = finish_out(c, o_g))) return st;
   if (K > 0 && (st = finish_out(c, o_hv))) return st;
   if (phi_user) CU_TRY(cudaMemcpyAsync(phi_user, phi_d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -710,9 +743,6 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   }
   float tot = 0;
   cudaEventElapsedTime(&tot, ev0, ev1);
-  for (auto e : evs) cudaEventDestroy(e);
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
   c->launches = launches;
   c->stats.kernel_launches = launches;
   c->stats.graph_launches = graph_launches;
@@ -750,7 +780,7 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
   if (k.sponge < R) return bad(HV_EINVAL, "sponge must be >= 4 cells");
   if (!k.src_iz || !k.src_ix || !k.rec_iz || !k.rec_ix || !k.wavelet) return bad(HV_EINVAL, "null geometry");
   const int sb = k.src_begin, se = k.src_end ? k.src_end : k.nsrc;
-  if (sb < 0 || se > k.nsrc || sb >= se) return bad(HV_EINVAL, "bad shot shard");
+  if (sb < 0 || se > k.nsrc || sb > se) return bad(HV_EINVAL, "bad shot shard");  // empty shard allowed
   c->cfg.src_end = se;
   c->nloc = se - sb;
   for (int i = 0; i < k.nsrc; ++i)
@@ -767,6 +797,7 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
   c->cfg.src_iz = c->cfg.src_ix = c->cfg.rec_iz = c->cfg.rec_ix = nullptr;
   c->cfg.wavelet = nullptr;
   c->dev = k.device;
+  c->nccl_comm = k.nccl_comm;
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= k.device || k.device < 0) {
@@ -911,6 +942,7 @@ int hv_destroy(hv_ctx* c) {
   cudaFree(c->d_trecx_beg);
   cudaFree(c->d_trecx_id);
   cudaFree(c->d_src_amp);
+  if (c->ev_legacy) cudaEventDestroy(c->ev_legacy);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
   return HV_OK;
@@ -922,9 +954,31 @@ int hv_set_stream(hv_ctx* c, void* s) {
   return HV_OK;
 }
 
+int hv_set_comm(hv_ctx* c, void* comm) {
+  if (!c) return HV_ESTATE;
+  c->nccl_comm = comm;
+  c->cfg.nccl_comm = comm;
+  return HV_OK;
+}
+
 int hv_forward(hv_ctx* c, const float* m, float* d) {
   if (!c) return HV_ESTATE;
   return run(c, W_FORWARD, m, nullptr, 0, nullptr, d, nullptr, nullptr, nullptr);
+}
+
+int hv_forward_shot(hv_ctx* c, const float* m, int32_t isrc, float* d) {
+  if (!c) return HV_ESTATE;
+  const int lo = isrc - c->cfg.src_begin;
+  if (lo < 0 || lo >= c->nloc)
+    return fail(c, HV_EINVAL, "shot " + std::to_string(isrc) + " is not in this context's shard [" +
+                                  std::to_string(c->cfg.src_begin) + ", " + std::to_string(c->cfg.src_end) + ")");
+  return run(c, W_FORWARD, m, nullptr, 0, nullptr, d, nullptr, nullptr, nullptr, lo, lo + 1);
+}
+
+int hv_misfit(hv_ctx* c, const float* m, const float* d_obs, double* phi) {
+  if (!c) return HV_ESTATE;
+  if (!phi) return fail(c, HV_EINVAL, "null pointer: phi");
+  return run(c, W_MISFIT, m, d_obs, 0, nullptr, nullptr, nullptr, phi, nullptr);
 }
 
 int hv_gradient(hv_ctx* c, const float* m, const float* d_obs, float* g, double* phi) {

@@ -53,6 +53,8 @@ struct hv_ctx {
   hv_stats stats{};
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   int64_t launches = 0;
+  cudaEvent_t ev_legacy = nullptr;  // orders calls on the own stream after the legacy default stream (enter)
+  void* nccl_comm = nullptr;        // optional ncclComm_t: in-library all-reduce of g / H·v / phi (hv_set_comm)
 };
 
 namespace hvrt {
@@ -68,6 +70,12 @@ bool is_device_ptr(const void* p);
 int stage_in(hv_ctx* c, const char* name, const void* p, size_t bytes, const void** dev);
 int stage_out(hv_ctx* c, const char* name, void* p, size_t bytes, OutStage* o);
 int finish_out(hv_ctx* c, const OutStage& o);
+// Entry of every public call: selects the device and, when no stream is bound (the context's own non-blocking
+// stream), makes the call wait for the work already queued on the legacy default stream (torch's default stream).
+int enter(hv_ctx* c);
+// In-library NCCL (dlopen'ed libnccl.so.2; no link-time dependency): sum-all-reduce on the context's stream.
+// dtype: 0 float32, 1 float64. Returns HV_OK, or HV_ENCCL with the detail in the context.
+int nccl_allreduce_sum(hv_ctx* c, void* buf, size_t count, int dtype);
 }  // namespace hvrt
 
 #define CU_TRY(call)                                                                           \

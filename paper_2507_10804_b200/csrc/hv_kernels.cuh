@@ -1212,8 +1212,11 @@ __global__ void __launch_bounds__(NTHREADS, MINB)
 // ------------------------------------------------------------------------------------------------ helpers
 
 // a0: padded coefficient planes from the interior model m (edge-replicated into the sponge, C13).
+// vmax_bits: atomicMax of the float bits (finite positive values order like their bits; NaN / negative values
+// exceed +inf); vmin_bits: atomicMin of the bits read as int (any value <= 0 gives an int <= 0).
 __global__ void model_setup_kernel(Geo g, const float* __restrict__ m, float dt2_h2, float two_dt2_h2,
-                                   float* __restrict__ W2, float* __restrict__ imgc, unsigned int* vmax_bits) {
+                                   float* __restrict__ W2, float* __restrict__ imgc, unsigned int* vmax_bits,
+                                   int* vmin_bits) {
   const long long n = static_cast<long long>(g.Nz) * g.P;
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n;
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -1223,7 +1226,10 @@ __global__ void model_setup_kernel(Geo g, const float* __restrict__ m, float dt2
       const int iz = min(max(I - g.W, 0), g.nz - 1), ix = min(max(J - g.W, 0), g.nx - 1);
       const float v = m[static_cast<long long>(iz) * g.nx + ix];
       wv = dt2_h2 * v * v;
-      if (I == iz + g.W && J == ix + g.W) atomicMax(vmax_bits, __float_as_uint(v));
+      if (I == iz + g.W && J == ix + g.W) {
+        atomicMax(vmax_bits, __float_as_uint(v));
+        atomicMin(vmin_bits, __float_as_int(v));
+      }
     }
     W2[q] = wv;
   }
@@ -1289,9 +1295,11 @@ __global__ void gather_last_kernel(Geo g, const float* __restrict__ pool, int ns
   }
 }
 
-// K4: residual rho = d - d_obs and phi = 1/2 sum rho^2 in float64.
+// K4: residual rho = d - d_obs and the block partials of phi = 1/2 sum rho^2 in float64 (part[blockIdx.x]); with
+// a fixed grid every partial sums the same elements in the same order, and phi_reduce_kernel adds them in index
+// order: phi is bit-deterministic.
 __global__ void residual_kernel(long long n, const float* __restrict__ d, const float* __restrict__ dobs,
-                                float* __restrict__ res, double* phi) {
+                                float* __restrict__ res, double* part) {
   double acc = 0.0;
   for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n;
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -1306,8 +1314,16 @@ __global__ void residual_kernel(long long n, const float* __restrict__ d, const 
   if (threadIdx.x < 32) {
     double v = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) atomicAdd(phi, v);
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
   }
+}
+
+// phi += sum_b part[b] (one warp, fixed order: lane l sums b = l, l + 32, ..., then a fixed butterfly).
+__global__ void phi_reduce_kernel(const double* __restrict__ part, int nb, double* phi) {
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nb; b += 32) v += part[b];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (threadIdx.x == 0) *phi += v;
 }
 
 // a8 within a GPU: out[f][iz][ix] = sum_s acc[s][slot f][iz + W][ix + W] in a fixed order (deterministic).

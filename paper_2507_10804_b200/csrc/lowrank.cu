@@ -70,7 +70,7 @@ extern "C" int hv_lowrank_geneig(hv_ctx* c, const float* m, int32_t r, int32_t K
   if (r < 1 || K < r || power_iters < 0) return fail(c, HV_EINVAL, "need 1 <= r <= K, power_iters >= 0");
   if (!(delta > 0.0) || !(gamma >= 0.0)) return fail(c, HV_EINVAL, "delta must be > 0, gamma >= 0");
   if (!evals_user) return fail(c, HV_EINVAL, "null evals");
-  CU_TRY(cudaSetDevice(c->dev));
+  if (const int e_ = hvrt::enter(c)) return e_;
   const int nz = c->g.nz, nx = c->g.nx;
   const long long N = (long long)nz * nx;
   const double h = c->cfg.h;

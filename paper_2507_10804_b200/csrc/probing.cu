@@ -182,7 +182,7 @@ int hv_psf_rows(hv_ctx* c, int32_t nz, int32_t nx, int32_t nb, const float* resp
   if (!is_device_ptr(pt_batch))
     for (int k = 0; k < np; ++k)
       if (pt_batch[k] < 0 || pt_batch[k] >= nb) return fail(c, HV_EINVAL, "point batch index out of range");
-  CU_TRY(cudaSetDevice(c->dev));
+  if (const int e_ = hvrt::enter(c)) return e_;
   const long long n = (long long)nz * nx;
   const float* R;
   const int *iz, *ix, *pb;
@@ -207,7 +207,7 @@ int hv_psf_weights(hv_ctx* c, int32_t nz, int32_t nx, int32_t nlz, const int32_t
   if (!c) return HV_ESTATE;
   c->err.clear();
   if (nz < 1 || nx < 1 || nlz < 1 || nlx < 1) return fail(c, HV_EGRID, "bad sizes");
-  CU_TRY(cudaSetDevice(c->dev));
+  if (const int e_ = hvrt::enter(c)) return e_;
   const int *lz, *lx;
   int st;
   if ((st = stage_in(c, "lat_z", lat_z, sizeof(int) * nlz, (const void**)&lz))) return st;
@@ -231,7 +231,7 @@ int hv_pdo_columns(hv_ctx* c, int32_t nz, int32_t nx, const float* response, int
   c->err.clear();
   if (nz < 1 || nx < 1 || r < 1) return fail(c, HV_EGRID, "bad sizes");
   if (!(mask_radius >= 0.0f)) return fail(c, HV_EINVAL, "bad mask radius");
-  CU_TRY(cudaSetDevice(c->dev));
+  if (const int e_ = hvrt::enter(c)) return e_;
   const long long n = (long long)nz * nx;
   const float* R;
   const int *kz, *kx;
@@ -260,7 +260,7 @@ int hv_pdo_weights(hv_ctx* c, int32_t nz, int32_t nx, float h, float rho0, int32
   c->err.clear();
   if (nz < 1 || nx < 1 || r < 2 || (r % 2)) return fail(c, HV_EINVAL, "r must be even and >= 2");
   if (!(h > 0.0f) || !(rho0 > 0.0f)) return fail(c, HV_EINVAL, "h and rho0 must be positive");
-  CU_TRY(cudaSetDevice(c->dev));
+  if (const int e_ = hvrt::enter(c)) return e_;
   const long long n = (long long)nz * nx;
   const float* th;
   int st;

@@ -94,7 +94,7 @@ extern "C" int hv_psf_plus(hv_ctx* c, int32_t nz, int32_t nx, int32_t nr, const 
   if (nz < 1 || nx < 1 || nr < 1 || nc < 1) return fail(c, HV_EGRID, "bad sizes");
   if (rank < 1 || rank > nr) return fail(c, HV_EINVAL, "need 1 <= rank <= nr");
   if (!col_kz || !col_kx) return fail(c, HV_EINVAL, "null column indices");
-  CU_TRY(cudaSetDevice(c->dev));
+  if (const int e_ = hvrt::enter(c)) return e_;
   const long long N = (long long)nz * nx;
   std::vector<int> ic(nc);
   {

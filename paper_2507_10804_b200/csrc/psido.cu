@@ -135,7 +135,7 @@ extern "C" int hv_psido_apply(hv_ctx* c, int32_t nz, int32_t nx, int32_t r, cons
   const int ca = (mode & 4) ? 1 : 0;  // complex spatial factors (PSF+)
   mode &= 3;
   if (mode > 2) return fail(c, HV_EINVAL, "mode must be 0, 1 or 2 (+4 for complex a)");
-  CU_TRY(cudaSetDevice(c->dev));
+  if (const int e_ = hvrt::enter(c)) return e_;
   const long long n = (long long)nz * nx;
   const float *a, *b, *v;
   int st;
@@ -185,7 +185,7 @@ extern "C" int hv_highpass(hv_ctx* c, int32_t nz, int32_t nx, float h, float cut
   c->err.clear();
   if (nz < 1 || nx < 1 || K < 1) return fail(c, HV_EGRID, "bad sizes");
   if (!(h > 0.0f) || !(width > 0.0f) || !(cutoff >= 0.0f)) return fail(c, HV_EINVAL, "bad filter parameters");
-  CU_TRY(cudaSetDevice(c->dev));
+  if (const int e_ = hvrt::enter(c)) return e_;
   const long long n = (long long)nz * nx;
   const float* v;
   int st;

@@ -1,6 +1,8 @@
-"""World-size-2 gloo test of the multi-GPU path's host logic on CPU: contiguous shot shards,
-rank-local partial sums, one all-reduce. The per-rank partial sums come from the fp64 oracle standing in for
-the GPU solver (test infrastructure), so this checks the partition and the reduction, not the kernels."""
+"""gloo tests of the multi-GPU path's host logic on CPU: contiguous shot shards, probe split
+when there are fewer shots than ranks, empty shards, rank-local partial sums, one all-reduce -- through
+`ShardedOperator`, the code path bench.py runs. The per-rank partial sums come from the fp64 oracle standing in
+for the GPU solver (test infrastructure), so this checks the partition and the reduction, not the kernels
+(tests/test_gpu_dist.py runs the real Solver through the same operator on cuda:0)."""
 import os
 import socket
 
@@ -10,7 +12,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2507_10804_b200.dist import ShardedOperator, shard_range
+from paper_2507_10804_b200.dist import ShardedOperator, plan_shards, shard_range
 
 
 def test_shard_range_partitions():
@@ -26,6 +28,17 @@ def test_shard_range_partitions():
         shard_range(4, 2, 2)
 
 
+@pytest.mark.parametrize("ns,K,world", [(3, 2, 2), (64, 32, 8), (2, 5, 8), (2, 3, 3), (1, 1, 4), (5, 7, 4)])
+def test_plan_shards_covers_every_pair_once(ns, K, world):
+    cover = np.zeros((ns, K), dtype=int)
+    grad = np.zeros(ns, dtype=int)
+    for sh in plan_shards(ns, K, world):
+        cover[sh.s0:sh.s1, sh.k0:sh.k1] += 1
+        if sh.grad:
+            grad[sh.s0:sh.s1] += 1
+    assert np.all(cover == 1) and np.all(grad == 1)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -34,13 +47,18 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, outdir):
+def _case(ns):
     import workloads as W
+    return W.custom(10, 14, nt=60, W=6, ns=ns, n_probes=3, f_peak=20.0, seed=4)
+
+
+def _worker(rank, world, port, outdir, ns):
     from oracle import wave
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-    wl = W.custom(10, 14, nt=60, W=6, ns=3, n_probes=2, f_peak=20.0, seed=4)
+    wl = _case(ns)
     pb = wave.Problem(wl)
-    b, e = shard_range(wl.ns, world, rank)
+    sh = plan_shards(wl.ns, wl.n_probes, world)[rank]
+    b, e = sh.s0, sh.s1
     V = wl.probes().astype(np.float64)
     d_obs = wave.Problem(wl, wl.model_true).forward_all()
 
@@ -51,9 +69,9 @@ def _worker(rank, world, port, outdir):
         phi, g = pb.gradient(dloc, shots=range(b, e))
         return phi, torch.from_numpy(g)
 
-    op = ShardedOperator(partial_hessvec, partial_gradient)
-    HV = op.hessvec(None, torch.from_numpy(V))
-    phi, g = op.gradient(None, d_obs[b:e])
+    op = ShardedOperator(partial_hessvec, partial_gradient, shard=sh)
+    HV = op.hessvec(torch.zeros(wl.nz, wl.nx, dtype=torch.float64), torch.from_numpy(V))
+    phi, g = op.gradient(torch.zeros(wl.nz, wl.nx, dtype=torch.float64), d_obs[b:e])
     if rank == 0:
         np.save(os.path.join(outdir, "hv.npy"), HV.numpy())
         np.save(os.path.join(outdir, "g.npy"), g.numpy())
@@ -62,12 +80,13 @@ def _worker(rank, world, port, outdir):
     dist.destroy_process_group()
 
 
-def test_two_rank_gloo_sum_equals_single_process(tmp_path):
-    import workloads as W
+@pytest.mark.parametrize("ns,world", [(3, 2), (1, 2)])
+def test_two_rank_gloo_sum_equals_single_process(tmp_path, ns, world):
+    """(3 shots, 2 ranks): shot shards; (1 shot, 2 ranks): probe split (rank 0 rows 0-1, rank 1 row 2)."""
     from oracle import wave
     port = _free_port()
-    mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
-    wl = W.custom(10, 14, nt=60, W=6, ns=3, n_probes=2, f_peak=20.0, seed=4)
+    mp.spawn(_worker, args=(world, port, str(tmp_path), ns), nprocs=world, join=True)
+    wl = _case(ns)
     pb = wave.Problem(wl)
     ref = pb.hessvec(list(wl.probes().astype(np.float64)))
     d_obs = wave.Problem(wl, wl.model_true).forward_all()

@@ -2,8 +2,8 @@
 
 Bar (BASELINE.json north_star): relative L2 <= 1e-4 on d, g and H·v. Cases span several 64x32 tiles
 with ragged tails, every storage mode, several shot batches and field groupings, and full BASELINE
-sizes in the bench's launch configuration (a sampled shot/probe slice against the oracle, plus
-properties that hold at any size)."""
+sizes (properties that hold at any size here; the bench's exact launch plans against oracle golden rows
+in tests/test_gpu_golden.py)."""
 import numpy as np
 import pytest
 
@@ -272,21 +272,6 @@ def test_errors(hv):
 # ---------------------------------------------------------------------------------------------- full size
 
 
-def test_cfg1_full_size_sampled_slice(hv):
-    """BASELINE cfg 1 at full size (201 x 401, nt = 2000) in the bench's launch configuration:
-    shot 7 with PSF probes (3,3) and (6,2) against the oracle (SURVEY.md §8(d) parity sub-slice)."""
-    wl = W.config(1)
-    ks = [3 * 8 + 3, 6 * 8 + 2]
-    V = wl.probes(ks)
-    s = hv.Solver.from_workload(wl, src_begin=7, src_end=8)
-    out = s.hessvec(wl.model, V)
-    pb = wave.Problem(wl)
-    ref = pb.hessvec(list(V.astype(np.float64)), shots=[7], mode="checkpoint", ckpt=45)
-    assert rel_l2(out, ref) <= TOL, rel_l2(out, ref)
-    d7 = s.forward(wl.model)[0]
-    assert rel_l2(d7, pb.forward(7)) <= TOL
-
-
 def test_cfg1_full_batch_properties(hv):
     """All 16 shots x 64 PSF spikes (the bench workload): H symmetric on the spike lattice,
     HV_i(x_j) = HV_j(x_i) (self-adjoint), PSD diagonal, and batching invariance."""
@@ -323,44 +308,10 @@ def test_psido_apply_parity(hv, nz, nx, r):
         assert rel_l2(out, ref) <= TOL, (mode, rel_l2(out, ref))
 
 
-# ---------------------------------------------------------------------------------------------- cfg 2 / 3 / 4
-# Full BASELINE grids in their launch configurations, against the oracle on the SURVEY.md §8(d) parity
-# sub-slices. The time axis is truncated (the fp64 numpy oracle needs ~18 ms per field-step on the 424 x 1192
-# cfg 2 grid and ~0.45 s on the 2088 x 6184 cfg 4 grid); the full-length runs are covered by the properties above.
-
-
-@pytest.fixture(scope="module")
-def cfg2_slice_ref():
-    wl = W.config(2).subset(shots=[31], nt=300)
-    V = wl.probes([0, 1])
-    # R-grad: at nt = 300 only the direct wave in the water has arrived, identical for m and
-    # v_true, so the gradient is evaluated at a 4 % slow start model where the residual is O(|d|)
-    m0 = (0.96 * wl.model).astype(np.float32)
-    pb = wave.Problem(wl, m0)
-    d_obs = wave.Problem(wl, wl.model_true).forward_all().astype(np.float32)
-    phi, g = pb.gradient(d_obs, mode="checkpoint", ckpt=17)
-    HV = pb.hessvec(list(V.astype(np.float64)), mode="checkpoint", ckpt=17)
-    return wl, V, m0, d_obs, phi, g, HV
-
-
-@pytest.mark.parametrize("store", ["full", "checkpoint", "boundary"])
-def test_cfg2_full_grid_fused_gradient_hessvec_slice(hv, cfg2_slice_ref, store):
-    wl, V, m0, d_obs, phi, g, HV = cfg2_slice_ref
-    s = hv.Solver.from_workload(wl, store=store)
-    phig, gg, hvg = s.gradient_hessvec(m0, d_obs, V)
-    assert rel_l2(gg, g) <= TOL, rel_l2(gg, g)
-    assert rel_l2(hvg, HV) <= TOL, rel_l2(hvg, HV)
-    assert abs(phig - phi) <= PHI_TOL * phi
-
-
-def test_cfg3_full_grid_pdo_probe_slice(hv):
-    """Rademacher probe k = 0 and cosine probe k = 16 (kappa = (1/16, 1/16), in band), shot 31."""
-    wl = W.config(3).subset(shots=[31], nt=300)
-    V = wl.probes([0, 16])
-    ref = wave.Problem(wl).hessvec(list(V.astype(np.float64)), mode="checkpoint", ckpt=17)
-    out = hv.Solver.from_workload(wl).hessvec(wl.model, V)
-    for k in range(2):
-        assert rel_l2(out[k], ref[k]) <= TOL, (k, rel_l2(out[k], ref[k]))
+# ---------------------------------------------------------------------------------------------- cfg 4
+# Full-nt oracle comparisons of the cfg 1 / 2 / 3 bench plans use committed golden rows (tests/test_gpu_golden.py).
+# The cfg 4 grid (2048 x 6144, 12.9 M padded points) is checked on a truncated time axis: the fp64 numpy oracle
+# needs ~0.5 s per field-step there.
 
 
 def test_cfg4_full_grid_checkpoint_slice(hv):

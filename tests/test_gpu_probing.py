@@ -1,5 +1,5 @@
 """GPU parity of probe -> symbol assembly against the fp64 oracle, on synthetic responses
-and end to end on real H·v responses: PSF rows from the cfg 1 spike H·v and PDO columns from a cosine-sum
+and end to end on real H·v responses: PSF rows from spike H·v on the cfg 0 model and PDO columns from a cosine-sum
 probe, assembled and applied through hv_psido_apply."""
 import math
 

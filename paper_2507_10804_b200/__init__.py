@@ -59,7 +59,7 @@ class HvStats(ctypes.Structure):
         ("shot_batch", ctypes.c_int32), ("field_group", ctypes.c_int32), ("store", ctypes.c_int32),
         ("ckpt_interval", ctypes.c_int32), ("bytes_per_shot", ctypes.c_double),
         ("ms_forward", ctypes.c_double), ("ms_backward", ctypes.c_double), ("ms_total", ctypes.c_double),
-        ("fwd_kernel", ctypes.c_int32),
+        ("fwd_kernel", ctypes.c_int32), ("bwd_kernel", ctypes.c_int32),
     ]
 
 

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhv.so")
 SOURCES = ["hv_api.cu", "hv_runtime.cu", "psido.cu", "probing.cu", "lowrank.cu", "psfplus.cu"]
-HEADERS = ["hv_kernels.cuh", "hv_fwd2.cuh", "hv_bwd2.cuh", "hv_geo.h", "hv_internal.h", os.path.join("..", "..", "include", "hv.h")]
+HEADERS = ["hv_kernels.cuh", "hv_t2.cuh", "hv_geo.h", "hv_internal.h", os.path.join("..", "..", "include", "hv.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -24,8 +24,7 @@
 #include "../../include/hv.h"
 #include "hv_internal.h"
 #include "hv_kernels.cuh"
-#include "hv_fwd2.cuh"
-#include "hv_bwd2.cuh"
+#include "hv_t2.cuh"
 
 using namespace hvk;
 using namespace hvrt;
@@ -47,7 +46,8 @@ int make_tmap(hv_ctx* c, const float* base, long long nplanes, int box_w, int bo
   return HV_OK;
 }
 
-constexpr bool kTwoStepDefault = false;
+constexpr bool kTwoStepDefault = false;  // T = 2 forward (fwd_t2_kernel) by default
+constexpr bool kT2BwdDefault = true;     // with it, the T = 2 adjoint (bwd_t2_kernel) for FULL-store calls
 constexpr int kPhiBlocks = 1024;  // residual kernel grid: fixed, so phi's summation order never changes
 constexpr int kQresFG = 6;  // resident-q forward: Born fields per CTA (6 q_k tiles + 3 stages: 2 CTAs per SM)
 // Backward CTAs per (tile, field group): the batch's shots are split into this many parts, each summing its
@@ -59,13 +59,13 @@ constexpr int kQresFG = 6;  // resident-q forward: Born fields per CTA (6 q_k ti
 #endif
 constexpr int kBwdSplit = HV_BWD_SPLIT;
 
-// 3-D tensor map over interior planes [nplanes][nz][PI] (the imaging-factor stores), box TX x TZ.
-int make_tmap_interior(hv_ctx* c, const float* base, long long nplanes, CUtensorMap* map) {
+// 3-D tensor map over interior planes [nplanes][nz][PI] (the imaging-factor stores), box bw x bh.
+int make_tmap_interior(hv_ctx* c, const float* base, long long nplanes, CUtensorMap* map, int bw = TX, int bh = TZ) {
   const Geo& g = c->g;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.PI), static_cast<cuuint64_t>(g.nz),
                         static_cast<cuuint64_t>(nplanes)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.PI) * 4, static_cast<cuuint64_t>(g.iplane) * 4};
-  cuuint32_t box[3] = {static_cast<cuuint32_t>(TX), static_cast<cuuint32_t>(TZ), 1};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = c->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -100,7 +100,7 @@ struct Plan {
   int S = 1;           // shots in flight
   int FG = 8;
   int nslot = 1;       // field slots per shot: 0 = background / residual adjoint, 1..K Born / adjoint, K+1 replay
-  int nlev = 2;        // pool planes per slot: 2 (parity, single-step kernels) or 4 (two-step forward, fwd2)
+  int nlev = 2;        // pool planes per slot: 2 (parity, single-step kernels) or 4 (T = 2 forward, fwd_t2)
   int nacc = 0;        // accumulator slots
   double per_shot = 0; // bytes
 };
@@ -128,7 +128,7 @@ int plan_call(hv_ctx* c, int want, int K, int nloc, Plan* pl) {
   }
   double budget = c->cfg.mem_budget ? static_cast<double>(c->cfg.mem_budget)
                                     : 0.9 * (static_cast<double>(freeb) + held);
-  // two-step kernels (fwd2 / bwd2) for FULL-store and forward-only calls; HV_T2=0 forces the single-step ones
+  // T = 2 forward (fwd_t2_kernel) for FULL-store and forward-only calls; HV_T2=0/1 overrides the default
   const char* t2 = std::getenv("HV_T2");
   const bool t2_on = t2 ? std::strcmp(t2, "0") != 0 : kTwoStepDefault;
   // shared (not per shot): Q, W2, imgc, rec coef, staging of V/HV/m
@@ -154,7 +154,7 @@ int plan_call(hv_ctx* c, int want, int K, int nloc, Plan* pl) {
   if (store != HV_STORE_FULL && store != HV_STORE_CHECKPOINT && store != HV_STORE_BOUNDARY)
     return fail(c, HV_EINVAL, "unknown storage mode " + std::to_string(store));
   pl->store = store;
-  pl->nlev = (store == HV_STORE_FULL && t2_on) ? 4 : 2;
+  pl->nlev = (store == HV_STORE_FULL && t2_on) ? 4 : 2;  // forward-only calls plan store = FULL (nothing kept)
   pl->k = k;
   pl->nck = (g.nt - 1 + k - 1) / k;
   pl->per_shot = per_shot(store, k);
@@ -304,6 +304,9 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   const long long ringN = ring_size(g);
   const long long planes_per_shot = static_cast<long long>(pl.nlev) * nslot;
   const bool use_t2 = pl.nlev == 4;
+  // T = 2 adjoint for FULL-store calls (HV_T2B=0/1 overrides; it needs the 4-plane pool of the T = 2 plan)
+  bool use_t2b = use_t2 && pl.store == HV_STORE_FULL && kT2BwdDefault;
+  if (const char* e = std::getenv("HV_T2B")) use_t2b = use_t2 && pl.store == HV_STORE_FULL && std::strcmp(e, "0") != 0;
   if ((st = ws_get(c, "pool", sizeof(float) * g.plane * planes_per_shot * S, (void**)&pool))) return st;
   if (K > 0 && (st = ws_get(c, "dborn", sizeof(float) * (size_t)S * K * g.nt * g.nrec, (void**)&dborn))) return st;
   double* phi_part = nullptr;  // per-block partial sums of the residual kernel (fixed-order phi, no atomics)
@@ -331,8 +334,15 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   if ((st = make_tmap(c, Q ? Q : pool, Q ? K : planes_per_shot * S, TX, TZ, &map_q))) return st;
   CUtensorMap map_w;
   if ((st = make_tmap(c, W2, 1, TX, TZ, &map_w))) return st;
+  CUtensorMap map_halo_t2, map_mid_t2, map_q_t2;  // T = 2 forward boxes: 72 x 72 halo, 64 x 64 mid region
+  if (use_t2) {
+    if ((st = make_tmap(c, pool, planes_per_shot * S, T2_IX, T2_IZ, &map_halo_t2))) return st;
+    if ((st = make_tmap(c, pool, planes_per_shot * S, T2_MX, T2_MZ, &map_mid_t2))) return st;
+    if ((st = make_tmap(c, Q ? Q : pool, Q ? K : planes_per_shot * S, T2_MX, T2_MZ, &map_q_t2))) return st;
+  }
   // s^j tensor map of the backward (FULL store / BOUNDARY level buffer / CHECKPOINT segment)
-  CUtensorMap map_sj = map_tile;
+  CUtensorMap map_sj = map_tile, map_s_t2 = map_tile;
+  if (adjoint && use_t2b && (st = make_tmap_interior(c, store, (long long)S * g.nt, &map_s_t2, OX, OZ))) return st;
   if (adjoint) {
     if (pl.store == HV_STORE_FULL) st = make_tmap_interior(c, store, (long long)S * g.nt, &map_sj);
     else if (pl.store == HV_STORE_BOUNDARY) st = make_tmap_interior(c, sbuf, 2LL * S, &map_sj);
@@ -375,7 +385,10 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   // One shot batch = one enqueue of the whole time loop (forward sweep, checkpoint saves / replays, backward
   // sweep). It is captured once into a CUDA graph per (call signature, buffers) and replayed afterwards.
   int64_t batch_launches = 0;
-  int fwd_kernel_used = 0;
+  // forward sweep kernel (decided here, not inside enqueue_batch: replayed graphs never re-run the lambda)
+  bool qres_call = K > 0 && 4.0 * K * g.plane > 48e6;
+  if (const char* qe = std::getenv("HV_QRES")) qres_call = K > 0 && std::strcmp(qe, "0") != 0;
+  const int fwd_kernel_used = use_t2 ? 3 : (qres_call ? 1 : 0);
   // phase 0: forward sweep (+ gather); phase 1: backward sweep. Events may be null (recorded by the caller).
   auto enqueue_batch = [&](int phase, int b0, int Sb, cudaEvent_t e_f0, cudaEvent_t e_f1, cudaEvent_t e_b0,
                            cudaEvent_t e_b1) -> int {
@@ -425,49 +438,44 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     if (const char* sbe = std::getenv("HV_SBLK")) fp.sblk = std::max(1, std::min(Sb, std::atoi(sbe)));  // tuning
     const dim3 gridf(fwd_grid(ntiles_all * Gf * Sb));
     // resident-q forward (q_k read once per launch) for Q too large for L2: HV_QRES=0/1 overrides (tuning)
-    bool qres = K > 0 && 4.0 * K * g.plane > 48e6;
-    if (const char* qe = std::getenv("HV_QRES")) qres = K > 0 && std::strcmp(qe, "0") != 0;
+    const bool qres = qres_call;
     fp.qfg = std::min(K > 0 ? K : 1, kQresFG);
     if (const char* qf = std::getenv("HV_QFG")) fp.qfg = std::max(1, std::min({K > 0 ? K : 1, 16, std::atoi(qf)}));
     const int Gq = K > 0 ? (K + fp.qfg - 1) / fp.qfg : 1;
     const int qres_smem = STAGES_BYTES + BAR_BYTES + fp.qfg * PT_BYTES;
-    fwd_kernel_used = use_t2 ? 2 : (qres ? 1 : 0);
     if (phase == 0 && use_t2) {
-      Fwd2Params f2{};
-      f2.g = g;
-      f2.nslot = nslot;
-      f2.pool = pool;
-      f2.born_slot0 = 1;
-      f2.K = K;
-      f2.S = Sb;
-      f2.G = Gf;
-      f2.W2 = W2;
-      f2.imgc = imgc;
-      f2.s_shot_stride = fp.s_shot_stride;
-      f2.shot0 = b0;
-      f2.src_I = c->d_srcI;
-      f2.src_J = c->d_srcJ;
-      f2.src_amp = c->d_src_amp;
-      f2.trec_beg = c->d_trec2_beg;
-      f2.trec_id = c->d_trec2_id;
-      f2.rec_I = c->d_recI;
-      f2.rec_J = c->d_recJ;
-      f2.d_bg = fp.d_bg;
-      f2.dbg_shot0 = fp.dbg_shot0;
-      f2.d_born = dborn;
-      int nb = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fwd2_kernel, BX * BY, F2_SMEM_BYTES) != cudaSuccess ||
-          nb < 1) {
-        cudaGetLastError();
-        nb = 1;
-      }
-      const long long units = static_cast<long long>(g.ntx2) * g.ntz2 * Gf * Sb;
-      const dim3 grid2(static_cast<unsigned>(std::max(1LL, std::min(static_cast<long long>(nb) * c->nsm, units))));
+      T2Params t2{};
+      t2.g = g;
+      t2.nslot = nslot;
+      t2.pool = pool;
+      t2.bg_update = 1;
+      t2.born_slot0 = 1;
+      t2.K = K;
+      t2.S = Sb;
+      t2.G = K > 0 ? (K + T2_QFG - 1) / T2_QFG : 1;
+      t2.ntx = g.ntx2;
+      t2.ntz = g.ntz2;
+      t2.W2 = W2;
+      t2.imgc = imgc;
+      t2.s_shot_stride = fp.s_shot_stride;
+      t2.shot0 = b0;
+      t2.src_I = c->d_srcI;
+      t2.src_J = c->d_srcJ;
+      t2.src_amp = c->d_src_amp;
+      t2.trec_beg = c->d_trec2_beg;
+      t2.trec_id = c->d_trec2_id;
+      t2.rec_I = c->d_recI;
+      t2.rec_J = c->d_recJ;
+      t2.d_bg = fp.d_bg;
+      t2.dbg_shot0 = fp.dbg_shot0;
+      t2.d_born = dborn;
+      const dim3 grid2(static_cast<unsigned>(t2.G * g.ntx2 * g.ntz2));
+      const dim3 block2(BX, T2_BY);
       for (int n = 0; n <= g.nt - 2; n += 2) {
-        f2.n = n;
-        f2.two = n + 2 <= g.nt - 1;
-        f2.s_out = full ? store + (size_t)n * g.iplane : nullptr;
-        fwd2_kernel<<<grid2, block, F2_SMEM_BYTES, c->stream>>>(map_halo, map_tile, map_q, f2);
+        t2.n = n;
+        t2.two = n + 2 <= g.nt - 1;
+        t2.s_out = full ? store + (size_t)n * g.iplane : nullptr;
+        fwd_t2_kernel<<<grid2, block2, t2_fwd_smem_bytes(), c->stream>>>(map_halo_t2, map_mid_t2, map_q_t2, t2);
         launches++;
       }
     } else if (phase == 0) {
@@ -546,37 +554,44 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
       if (e_b0) CU_TRY(cudaEventRecord(e_b0, c->stream));
       int cur_b = -1;
       int j_t1 = g.nt - 1;  // first level left for the single-step kernel
-      if (use_t2) {         // FULL store: two levels per launch, j = nt-1, nt-3, ... >= 2
-        Bwd2Params b2{};
+      if (use_t2b) {        // FULL store, T = 2 adjoint: levels j, j-1 per launch, j = nt-1, nt-3, ...
+        T2BwdParams b2{};
         b2.g = g;
         b2.nslot = nslot;
         b2.pool = pool;
         b2.slot0 = slot0_b;
         b2.F = Fb;
         b2.S = Sb;
+        b2.G = Gb;
+        b2.ntx = g.ntx2;
+        b2.ntz = g.ntz2;
         b2.W2 = W2;
-        b2.s_shot_stride = g.iplane * g.nt;
+        b2.sj_shot_planes = g.nt;
         b2.acc = acc;
         b2.rho_res = rres;
         b2.rho_born = dborn;
         b2.Kb = K;
         b2.rec_coef = rec_coef;
-        b2.trec_beg = c->d_trec2_beg;
-        b2.trec_id = c->d_trec2_id;
-        b2.trecx_beg = c->d_trecx_beg;
-        b2.trecx_id = c->d_trecx_id;
+        b2.tmid_beg = c->d_tmid_beg;
+        b2.tmid_id = c->d_tmid_id;
+        b2.tout_beg = c->d_trec2_beg;
+        b2.tout_id = c->d_trec2_id;
         b2.rec_I = c->d_recI;
         b2.rec_J = c->d_recJ;
-        const dim3 grid2(g.ntx2, g.ntz2, Gb);
-        int j = g.nt - 1;
-        for (; j >= 2; j -= 2) {
+        const dim3 gridb2(static_cast<unsigned>(Gb * g.ntx2 * g.ntz2));
+        const dim3 blockb2(BX, T2_BY);
+        for (int j = g.nt - 1; j >= 1; j -= 2) {
           b2.j = j;
-          b2.img_top = j <= g.nt - 2;
-          b2.s_lvl = store + (size_t)j * g.iplane;
-          bwd2_kernel<<<grid2, block, B2_SMEM_BYTES, c->stream>>>(map_halo, map_tile, b2);
+          b2.two = j - 1 >= 1;
+          b2.upd0 = j >= 2;
+          b2.upd1 = j - 1 >= 2;
+          b2.img0 = j <= g.nt - 2;
+          b2.img1 = j - 1 >= 1 && j - 1 <= g.nt - 2;
+          b2.sj_plane0 = j;
+          bwd_t2_kernel<<<gridb2, blockb2, t2_bwd_smem_bytes(), c->stream>>>(map_halo_t2, map_mid_t2, map_s_t2, b2);
           launches++;
         }
-        j_t1 = j;  // 1 (one level left: imaging only) or 0
+        j_t1 = 0;
       }
       for (int j = j_t1; j >= 1; --j) {
         bp.j = j;
@@ -755,6 +770,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   c->stats.ms_backward = ms_b;
   c->stats.ms_total = tot;
   c->stats.fwd_kernel = fwd_kernel_used;
+  c->stats.bwd_kernel = adjoint ? (use_t2b ? 3 : 0) : -1;
   return HV_OK;
 }
 
@@ -849,7 +865,7 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
     std::vector<int> fillp(beg.begin(), beg.end() - 1);
     for (int i = 0; i < k.nrec; ++i) ids[fillp[(rI[i] / TZ) * g.ntx + rJ[i] / TX]++] = i;
   }
-  // receivers owned by each output tile of the two-step forward kernel
+  // receivers owned by each output tile of the T = 2 forward kernel
   const int ntiles2 = g.ntx2 * g.ntz2;
   std::vector<int> beg2(ntiles2 + 1, 0), ids2(k.nrec);
   for (int i = 0; i < k.nrec; ++i) beg2[(rI[i] / OZ) * g.ntx2 + rJ[i] / OX + 1]++;
@@ -858,14 +874,14 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
     std::vector<int> fillp(beg2.begin(), beg2.end() - 1);
     for (int i = 0; i < k.nrec; ++i) ids2[fillp[(rI[i] / OZ) * g.ntx2 + rJ[i] / OX]++] = i;
   }
-  // receivers inside each two-step tile's ext region (core + R cells): level-j injection of the two-step adjoint
-  std::vector<int> begx(ntiles2 + 1, 0), idsx;
+  // receivers inside the mid region (output tile + R cells) of each T = 2 tile: injection into the mid level
+  std::vector<int> begm(ntiles2 + 1, 0), idsm;
   for (int t = 0; t < ntiles2; ++t) {
     const int tz = t / g.ntx2, txx = t % g.ntx2;
     const int z0 = tz * OZ - R, x0 = txx * OX - R;
     for (int i = 0; i < k.nrec; ++i)
-      if (rI[i] >= z0 && rI[i] < z0 + TZ && rJ[i] >= x0 && rJ[i] < x0 + TX) idsx.push_back(i);
-    begx[t + 1] = static_cast<int>(idsx.size());
+      if (rI[i] >= z0 && rI[i] < z0 + OZ + 2 * R && rJ[i] >= x0 && rJ[i] < x0 + OX + 2 * R) idsm.push_back(i);
+    begm[t + 1] = static_cast<int>(idsm.size());
   }
   std::vector<float> amp(k.nt);
   for (int n = 0; n < k.nt; ++n)
@@ -882,8 +898,8 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
       !up((void**)&c->d_trec_id, ids.data(), sizeof(int) * ids.size()) ||
       !up((void**)&c->d_trec2_beg, beg2.data(), sizeof(int) * beg2.size()) ||
       !up((void**)&c->d_trec2_id, ids2.data(), sizeof(int) * ids2.size()) ||
-      !up((void**)&c->d_trecx_beg, begx.data(), sizeof(int) * begx.size()) ||
-      !up((void**)&c->d_trecx_id, idsx.data(), sizeof(int) * std::max<size_t>(1, idsx.size())) ||
+      !up((void**)&c->d_tmid_beg, begm.data(), sizeof(int) * begm.size()) ||
+      !up((void**)&c->d_tmid_id, idsm.data(), sizeof(int) * std::max<size_t>(1, idsm.size())) ||
       !up((void**)&c->d_src_amp, amp.data(), sizeof(float) * amp.size())) {
     cudaGetLastError();
     hv_destroy(c);
@@ -912,8 +928,10 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
           cudaSuccess ||
       cudaFuncSetAttribute(fwd_qres_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            STAGES_BYTES + BAR_BYTES + 16 * PT_BYTES) != cudaSuccess ||
-      cudaFuncSetAttribute(fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, F2_SMEM_BYTES) != cudaSuccess ||
-      cudaFuncSetAttribute(bwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, B2_SMEM_BYTES) != cudaSuccess ||
+      cudaFuncSetAttribute(fwd_t2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t2_fwd_smem_bytes()) !=
+          cudaSuccess ||
+      cudaFuncSetAttribute(bwd_t2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t2_bwd_smem_bytes()) !=
+          cudaSuccess ||
       cudaFuncSetAttribute(rev_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, REV_SMEM_BYTES) !=
           cudaSuccess) {
     cudaGetLastError();
@@ -939,8 +957,8 @@ int hv_destroy(hv_ctx* c) {
   cudaFree(c->d_trec_id);
   cudaFree(c->d_trec2_beg);
   cudaFree(c->d_trec2_id);
-  cudaFree(c->d_trecx_beg);
-  cudaFree(c->d_trecx_id);
+  cudaFree(c->d_tmid_beg);
+  cudaFree(c->d_tmid_id);
   cudaFree(c->d_src_amp);
   if (c->ev_legacy) cudaEventDestroy(c->ev_legacy);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);

@@ -47,7 +47,6 @@ constexpr int BSTAGE_FLOATS = TILE_FLOATS + 2 * PT_FLOATS;
 constexpr int BSTAGES_BYTES = NSTAGE * BSTAGE_FLOATS * 4;
 constexpr int BWD_SMEM_BYTES = BSTAGES_BYTES + BAR_BYTES;
 constexpr int REV_SMEM_BYTES = STAGES_BYTES + BAR_BYTES;  // BOUNDARY reverse kernel: halo + tile stages
-constexpr int B2_SMEM_BYTES = STAGES_BYTES + PT_FLOATS * 4 + BAR_BYTES;  // two-step adjoint: + mid
 
 // standard 8th-order central second-derivative weights (unscaled; h^-2 is folded into the coefficients)
 #define HV_A0 (-205.0f / 72.0f)
@@ -56,14 +55,12 @@ constexpr int B2_SMEM_BYTES = STAGES_BYTES + PT_FLOATS * 4 + BAR_BYTES;  // two-
 #define HV_A3 (8.0f / 315.0f)
 #define HV_A4 (-1.0f / 560.0f)
 
-// two-step forward kernel (hv_fwd2.cuh): the TX x TZ region is computed at level n+1, its OX x OZ core at n+2
-constexpr int OX = TX - 2 * R;
-constexpr int OZ = TZ - 2 * R;
-#ifndef HV_NSTAGE_F2
-#define HV_NSTAGE_F2 3
+// T = 2 forward kernel (hv_t2.cuh): OX x OZ output tiles, level n+1 on the (OX + 2R) x (OZ + 2R) mid region
+constexpr int OX = 56;
+#ifndef HV_T2_OZ
+#define HV_T2_OZ 56
 #endif
-constexpr int NSTAGE_F2 = HV_NSTAGE_F2;
-constexpr int F2_SMEM_BYTES = NSTAGE_F2 * FSTAGE_FLOATS * 4 + PT_FLOATS * 4 + BAR_BYTES;
+constexpr int OZ = HV_T2_OZ;  // 56 (512-thread CTAs, 1 per SM) or 24 (256-thread CTAs, 2 per SM)
 
 
 struct Geo {
@@ -72,7 +69,7 @@ struct Geo {
   int P;                // row pitch of padded planes (floats) >= ntx * TX and >= ntx2 * OX
   int PI, c0;           // interior-store row pitch and first padded column stored (c0 % 4 == 0)
   int ntx, ntz;         // tile grid (TX x TZ tiles: single-step kernels)
-  int ntx2, ntz2;       // tile grid of the two-step forward kernel (OX x OZ output tiles)
+  int ntx2, ntz2;       // tile grid of the T = 2 forward kernel (OX x OZ output tiles)
   long long plane;      // Nz * P
   long long iplane;     // nz * PI
   float kc;             // eta_max * dt / (2 W^2): c = kc (d_z^2 + d_x^2)

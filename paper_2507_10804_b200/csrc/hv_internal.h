@@ -42,8 +42,8 @@ struct hv_ctx {
   // persistent device arrays
   int *d_srcI = nullptr, *d_srcJ = nullptr, *d_recI = nullptr, *d_recJ = nullptr;
   int *d_trec_beg = nullptr, *d_trec_id = nullptr;
-  int *d_trec2_beg = nullptr, *d_trec2_id = nullptr;  // per output (core) tile of the two-step kernels
-  int *d_trecx_beg = nullptr, *d_trecx_id = nullptr;  // per ext region (core + R) of the two-step kernels
+  int *d_trec2_beg = nullptr, *d_trec2_id = nullptr;  // per OX x OZ output tile of the T = 2 kernels
+  int *d_tmid_beg = nullptr, *d_tmid_id = nullptr;    // per T = 2 tile: receivers inside its mid region
   float* d_src_amp = nullptr;
   // grow-only workspace
   std::map<std::string, hvrt::DevBuf> ws;

@@ -611,23 +611,12 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
 }
 
 // ------------------------------------------------------------------------------------------------ forward, resident q
-// Forward for large Q (the v3 schedule, kept for grids whose Q does not fit L2): one CTA per (tile, Born group)
-// loops over all the batch's shots; the group's q_k tiles are loaded into shared memory once and reused by every
-// shot (q_k is read from DRAM once per launch), the resident CTAs step through the shots in lockstep (halo
-// overlaps are L2 hits). Scalar arithmetic, a block barrier per item, 3-stage ring of halo + level n-1 tiles.
-__device__ __forceinline__ void lap_points_scalar(const float* __restrict__ t, int tx, int ty, float (&L)[RZ][4],
-                                                  float (&C)[RZ][4]) {
-  float2 L2[RZ][2], C2[RZ][2];
-  lap_points(t, tx, ty, L2, C2);
-#pragma unroll
-  for (int r = 0; r < RZ; ++r)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      L[r][2 * h] = L2[r][h].x, L[r][2 * h + 1] = L2[r][h].y;
-      C[r][2 * h] = C2[r][h].x, C[r][2 * h + 1] = C2[r][h].y;
-    }
-}
-
+// Forward for large Q (Q = K x plane does not fit L2: cfg 3, the cfg 4 grid): one CTA per (tile, group of qfg Born
+// fields) loops over all the batch's shots; the group's q_k tiles are loaded into shared memory once and reused by
+// every shot (q_k is read from DRAM once per launch), the resident CTAs step through the shots in lockstep (halo
+// overlaps are L2 hits). Same paired-fp32 (FFMA2) arithmetic as fwd_step_kernel (bit-identical fields); each warp
+// releases a stage on its own "empty" mbarrier and thread 0 refills the stage of item c - 1 once every warp has
+// released it, so warps drift instead of meeting at a block barrier per item.
 template <bool SP>
 __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUtensorMap* mt, const CUtensorMap* mq,
                                          const FwdParams& p, float* stages, float* qs, uint64_t* bars) {
@@ -641,10 +630,12 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
   const int par_n = p.n & 1, par_new = par_n ^ 1;
   const bool leader = (grp == 0) && p.bg_update;
   uint64_t* qbar = bars + NSTAGE;
+  uint64_t* empty = bars + NSTAGE + 1;                // per stage: one arrival per warp
 
   // producer (thread 0): next item (ps, pt) -> stage
   int ps = 0, pt = 0, issued = 0;
   Ring prod;
+  Ring ering;        // stage whose release the next refill waits for
   auto issue_next = [&]() {
     float* st = stages + prod.stage * STAGE_FLOATS;
     const bool upd = pt > 0 || leader;
@@ -672,11 +663,11 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
   const int J0 = x0 + tx * 4;
   const int so = ty * RZ * TX + tx * 4;                       // smem offset of this thread's first point
   const long long go = static_cast<long long>(I0) * g.P + J0;  // plane offset of this thread's first point
-  float w[RZ][4];
+  float2 w[RZ][2];
 #pragma unroll
   for (int r = 0; r < RZ; ++r) {
     const float4 wv = ldg4(p.W2 + static_cast<long long>(min(I0 + r, g.Nz - 1)) * g.P + J0);
-    w[r][0] = wv.x, w[r][1] = wv.y, w[r][2] = wv.z, w[r][3] = wv.w;
+    w[r][0] = lo2(wv), w[r][1] = hi2(wv);
   }
   bool row_ok[RZ];
 #pragma unroll
@@ -690,11 +681,15 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
   if (nf > 0) mbar_wait(qbar, 0);
 
   Ring cons;
+  int consumed = 0;
   auto release = [&]() {
-    __syncthreads();  // every thread is done with this stage
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[cons.stage]);  // this warp is done with the stage
     cons.advance();
-    if (tid == 0 && issued < nitems) {
-      fence_proxy_async();
+    // thread 0 refills the stage of item c - 1 (c = the item it just finished) once every warp released it
+    if (tid == 0 && ++consumed >= 2 && issued < nitems) {
+      mbar_wait(&empty[ering.stage], ering.phase);
+      ering.advance();
       issue_next();
     }
   };
@@ -714,14 +709,14 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
     if (row_ok[r]) st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
   };
 
-  float Lb[RZ][4];
+  float2 Lb[RZ][2];
   for (int s = 0; s < p.S; ++s) {
     // ---------------- background u of shot s: L u^n (kept for the Born sources), leader updates u
     {
       const float* st = stages + cons.stage * STAGE_FLOATS;
       mbar_wait(&bars[cons.stage], cons.phase);
-      float C[RZ][4];
-      lap_points_scalar(st, tx, ty, Lb, C);
+      float2 C[RZ][2];
+      lap_points(st, tx, ty, Lb, C);
       if (leader) {
         float* dst = p.pool + (static_cast<long long>(s * p.nslot + p.bg_slot) * 2 + par_new) * g.plane;
         const int sI = p.src_I[p.shot0 + s], sJ = p.src_J[p.shot0 + s];
@@ -730,7 +725,10 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
           const float4 pv = ld4(st + TILE_FLOATS + so + r * TX);
           float v[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) v[i] = dmp.upd1(r, i, C[r][i], f4(pv, i), w[r][i] * Lb[r][i]);
+          for (int h = 0; h < 2; ++h) {
+            const float2 u = dmp.upd(r, h, C[r][h], half2of(pv, h), mul2(w[r][h], Lb[r][h]));
+            v[2 * h] = u.x, v[2 * h + 1] = u.y;
+          }
           if (I0 + r == sI && sJ >= J0 && sJ < J0 + 4) {  // point source dt^2 s[n] / h^2 (/(1 + c))
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -753,11 +751,14 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
             const int iz = I0 + r - g.W;
             if (iz < 0 || iz >= g.nz) continue;
             const float4 ic = ldg4(p.imgc + static_cast<long long>(iz) * g.PI + jc);
-            float o[4];
+            const float2 o01 = mul2(lo2(ic), Lb[r][0]), o23 = mul2(hi2(ic), Lb[r][1]);
+            float o[4] = {o01.x, o01.y, o23.x, o23.y};
+            if (SP) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int ix = J0 + i - g.W;
-              o[i] = (!SP || (ix >= 0 && ix < g.nx)) ? f4(ic, i) * Lb[r][i] : 0.0f;
+              for (int i = 0; i < 4; ++i) {
+                const int ix = J0 + i - g.W;
+                if (ix < 0 || ix >= g.nx) o[i] = 0.0f;
+              }
             }
             st4(p.s_out + s * p.s_shot_stride + static_cast<long long>(iz) * g.PI + jc,
                 make_float4(o[0], o[1], o[2], o[3]));
@@ -772,8 +773,8 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
     for (int t = 0; t < nf; ++t) {
       const float* st = stages + cons.stage * STAGE_FLOATS;
       mbar_wait(&bars[cons.stage], cons.phase);
-      float L[RZ][4], C[RZ][4];
-      lap_points_scalar(st, tx, ty, L, C);
+      float2 L[RZ][2], C[RZ][2];
+      lap_points(st, tx, ty, L, C);
       float* dst = born_base + static_cast<long long>(t) * 2 * g.plane;
       const float* qk = qs + t * PT_FLOATS + so;
 #pragma unroll
@@ -782,8 +783,11 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
         const float4 qv = ld4(qk + r * TX);
         float v[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          v[i] = dmp.upd1(r, i, C[r][i], f4(pv, i), fmaf(f4(qv, i), Lb[r][i], w[r][i] * L[r][i]));
+        for (int h = 0; h < 2; ++h) {
+          const float2 u = dmp.upd(r, h, C[r][h], half2of(pv, h),
+                                   fma2(half2of(qv, h), Lb[r][h], mul2(w[r][h], L[r][h])));
+          v[2 * h] = u.x, v[2 * h + 1] = u.y;
+        }
         store_row(dst, r, v);
       }
       if (re > rb && p.d_born) sample(st, p.d_born + (static_cast<long long>(s) * p.K + fb + t) * data_stride);
@@ -810,6 +814,7 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
     tma_prefetch_desc(&mt);
     tma_prefetch_desc(&mq);
     for (int i = 0; i < NSTAGE + 1; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < NSTAGE; ++i) mbar_init(&bars[NSTAGE + 1 + i], NTHREADS / 32);  // empty: one per warp
     fence_mbar_init();
   }
   __syncthreads();
@@ -863,7 +868,9 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   const int nf = min(p.F, fb + BWD_FG) - fb;
   if (nf <= 0 || se <= sb) return;
   const int nitems = (se - sb) * nf;
-  const int par_in = (p.j + 1) & (p.nlev - 1), par_out = p.j & (p.nlev - 1);
+  // planes of lambda^{j+1} (halo), lambda^{j+2} (pointwise) and lambda^j (written): with 2 planes per field
+  // lambda^j overwrites lambda^{j+2} in place; with 4 (after T = 2 forward sweeps) they are distinct planes
+  const int par_in = (p.j + 1) & (p.nlev - 1), par_out = p.j & (p.nlev - 1), par_prev = (p.j + 2) & (p.nlev - 1);
   int ps = sb, pt = 0, issued = 0;
   Ring prod;
   auto issue_next = [&]() {
@@ -872,7 +879,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
     const bool with_sj = p.imaging && pt == 0;  // s^j of the shot travels with its first field's stage
     mbar_expect_tx(&bars[prod.stage], TILE_BYTES + (p.update ? PT_BYTES : 0) + (with_sj ? PT_BYTES : 0));
     tma_load_3d(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_in);
-    if (p.update) tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_out);
+    if (p.update) tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_prev);
     if (with_sj)  // interior store: padded (x0, z0) is interior (x0 - c0, z0 - W); outside -> TMA zero fill
       tma_load_3d(st + TILE_FLOATS + PT_FLOATS, msj, &bars[prod.stage], x0 - g.c0, z0 - g.W,
                   static_cast<int>(p.sj_plane0 + static_cast<long long>(ps) * p.sj_shot_planes));

@@ -170,27 +170,32 @@ def test_deterministic_and_batch_invariant(hv, ragged):
     assert np.array_equal(c[0], a[1])
 
 
-@pytest.mark.parametrize("nt", [300, 301])
-def test_two_step_kernels_bitwise_equal_single_step(hv, ragged, nt, monkeypatch):
-    """The two-step kernels (fwd2 / bwd2, FULL store) compute every field level with the single-step kernels'
-    exact per-point operations: d is bitwise identical with HV_T2=0 (single-step). The imaging sums add the two
-    levels of a launch per shot before the shot sum (the single-step kernel adds one level per launch), so g, phi
-    and H·v agree to fp32 summation-order rounding. Even and odd numbers of steps (nt - 1): with and without a
-    trailing single-level launch."""
-    wl, V, d, HV, d_obs, phi, g, m_start = ragged
-    wl = W.custom(70, 150, nt=nt, ns=3, nrec=37, n_probes=3, f_peak=15.0, seed=5)
-    d_obs = d_obs[:, :nt] if nt <= d_obs.shape[1] else np.pad(d_obs, ((0, 0), (0, nt - d_obs.shape[1]), (0, 0)))
+@pytest.mark.parametrize("nt,K", [(300, 3), (301, 7), (161, 9)])
+def test_t2_kernels_match_single_step(hv, nt, K, monkeypatch):
+    """The T = 2 forward (fwd_t2_kernel: two levels per launch, resident q_k, groups of <= 4 Born fields)
+    computes every level with the single-step kernels' exact per-point operations: d, the FULL store, and hence
+    g, phi and H·v are bitwise identical with HV_T2=0. Even and odd numbers of steps (nt - 1: a trailing
+    one-level launch), one and several Born-field groups; and against the oracle."""
+    wl = W.custom(70, 150, nt=nt, ns=3, nrec=37, n_probes=K, f_peak=15.0, seed=5)
+    V = wl.probes()
+    d_obs = np.zeros((wl.ns, wl.nt, wl.nrec), np.float32)
     out = {}
-    for t2 in ("1", "0"):
+    for t2, t2b in (("1", "0"), ("0", "0"), ("1", "1")):
         monkeypatch.setenv("HV_T2", t2)
-        s = hv.Solver.from_workload(wl, store="full", shot_batch=2, field_group=2)
-        out[t2] = (s.forward(wl.model), s.gradient(m_start, d_obs), s.hessvec(wl.model, V))
-    (d1, (p1, g1), h1), (d0, (p0, g0), h0) = out["1"], out["0"]
+        monkeypatch.setenv("HV_T2B", t2b)
+        s = hv.Solver.from_workload(wl, store="full", shot_batch=2)
+        out[t2 + t2b] = (s.forward(wl.model), s.gradient(wl.model, d_obs), s.hessvec(wl.model, V))
+        assert s.stats()["fwd_kernel"] == (3 if t2 == "1" else 0)
+        assert s.stats()["bwd_kernel"] == (3 if t2b == "1" else 0)
+    (d1, (p1, g1), h1), (d0, (p0, g0), h0) = out["10"], out["00"]
     assert np.array_equal(d1, d0)
-    assert abs(p1 - p0) <= 1e-12 * abs(p0)           # phi depends on d only (fp64 block sums, atomic order)
-    assert rel_l2(g1, g0) <= 1e-6 and rel_l2(h1, h0) <= 1e-6
-    if nt == 300:
-        assert rel_l2(h1, HV) <= TOL
+    assert p1 == p0 and np.array_equal(g1, g0) and np.array_equal(h1, h0)
+    # T = 2 adjoint: lambda levels bit-identical, imaging summed two levels per launch (fp32 summation order)
+    d2, (p2, g2), h2 = out["11"]
+    assert np.array_equal(d2, d0) and p2 == p0
+    assert rel_l2(g2, g0) <= 1e-6 and rel_l2(h2, h0) <= 1e-6
+    ref = wave.Problem(wl).hessvec(list(V.astype(np.float64)))
+    assert rel_l2(h1, ref) <= TOL and rel_l2(h2, ref) <= TOL
 
 
 @pytest.mark.parametrize("nz,nx,ns,K,fg,batch", [

@@ -11,6 +11,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges per call / sweep / reduction (SURVEY.md §5 tracing)
 
 #include <algorithm>
 #include <cmath>
@@ -79,6 +80,12 @@ int grid1d(long long n) { return static_cast<int>(std::min<long long>((n + 255) 
 // ------------------------------------------------------------------------------------------ the plan
 
 enum Want { W_FORWARD = 1, W_GRAD = 2, W_HESS = 4, W_MISFIT = 8 };
+
+// NVTX range for the lifetime of a scope (host-side markers of the call, its sweeps and its reductions).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // CUDA events of one call, destroyed on every return path.
 struct Events {
@@ -220,6 +227,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
         float* g_user, double* phi_user, float* hv_user, int lo = 0, int hi = -1) {
   if (!c) return HV_ESTATE;
   c->err.clear();
+  NvtxRange nv_call((want & W_HESS) ? ((want & W_GRAD) ? "hv_gradient_hessvec" : "hv_hessvec")
+                    : (want & W_GRAD) ? "hv_gradient" : (want & W_MISFIT) ? "hv_misfit" : "hv_forward");
   if (const int e_ = hvrt::enter(c)) return e_;
   const Geo& g = c->g;
   if (hi < 0) hi = c->nloc;
@@ -684,9 +693,10 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     for (int phase = 0; phase < 2; ++phase) {
       char keybuf[1024];
       std::snprintf(keybuf, sizeof keybuf,
-                    "ph%d w%d K%d S%d Sb%d b%d st%d k%d FG%d p%p W%p i%p Q%p db%p dg%p rr%p a%p s%p ck%p sg%p rg%p "
-                    "sb%p do%p od%p rc%p",
-                    phase, want, K, S, Sb, b0, pl.store, pl.k, FG, (void*)pool, (void*)W2, (void*)imgc, (void*)Q,
+                    "ph%d w%d K%d S%d Sb%d b%d st%d k%d FG%d nl%d fk%d bk%d p%p W%p i%p Q%p db%p dg%p rr%p a%p s%p "
+                    "ck%p sg%p rg%p sb%p do%p od%p rc%p",
+                    phase, want, K, S, Sb, b0, pl.store, pl.k, FG, pl.nlev, fwd_kernel_used, use_t2b ? 1 : 0,
+                    (void*)pool, (void*)W2, (void*)imgc, (void*)Q,
                     (void*)dborn, (void*)dbg, (void*)rres, (void*)acc, (void*)store, (void*)ckpt, (void*)seg,
                     (void*)ring, (void*)sbuf, (const void*)dobs, fwd ? o_d.dev : nullptr, (void*)rec_coef);
       auto it = c->graphs.find(keybuf);
@@ -716,6 +726,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
         it = c->graphs.emplace(keybuf, ge).first;
       }
       // per-sweep timing events are recorded around the graph launches (events inside graphs cannot be timed)
+      NvtxRange nv_sweep(phase == 0 ? "forward_sweep" : "backward_sweep");
       CU_TRY(cudaEventRecord(ev4[2 * phase], c->stream));
       CU_TRY(cudaGraphLaunch(it->second.exec, c->stream));
       CU_TRY(cudaEventRecord(ev4[2 * phase + 1], c->stream));
@@ -738,6 +749,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   CU_TRY(cudaGetLastError());
   // a8 across GPUs: with a communicator attached, sum g / H·v / phi over the ranks in-library (NCCL on this stream)
   if (c->nccl_comm && (grad || misfit || K > 0)) {
+    NvtxRange nv_red("nccl_allreduce");
     if (grad && (st = nccl_allreduce_sum(c, o_g.dev, (size_t)g.nz * g.nx, 0))) return st;
     if (K > 0 && (st = nccl_allreduce_sum(c, o_hv.dev, (size_t)K * g.nz * g.nx, 0))) return st;
     if ((st = nccl_allreduce_sum(c, phi_d, 1, 1))) return st;

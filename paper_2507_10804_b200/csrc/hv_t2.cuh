@@ -114,8 +114,8 @@ __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtenso
       mbar_expect_tx(qbar, nf * T2_MID_FLOATS * 4);
       for (int t = 0; t < nf; ++t) tma_load_3d(qs + t * T2_MID_FLOATS, mq, qbar, ex0, ez0, fb + t);
     }
-    // NSTAGE - 1 items in flight: the stage of item i - 1 is refilled at item i's barrier
-    while (issued < min(T2_NSTAGE - 1, nitems)) issue_next();
+    // NSTAGE items in flight: phase 2 reads no stage data, so item i's stage is refilled at item i's barrier
+    while (issued < min(T2_NSTAGE, nitems)) issue_next();
   }
 
   const int I0 = ez0 + ty * RZ;
@@ -162,13 +162,20 @@ __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtenso
     }
     st4(mid + so + r * T2_MX, make_float4(v[0], v[1], v[2], v[3]));
   };
-  // d[n] from the staged halo of level n, d[n+1] from mid (receivers of this output tile)
-  auto sample = [&](const float* st, const float* mid, float* out) {
+  // d[n] from the staged halo of level n (before the barrier: the stage is refilled at it), d[n+1] from mid
+  auto sample_n = [&](const float* st, float* out) {
     for (int q = rb + tid; q < re; q += T2_NT) {
       const int rid = p.trec_id[q];
       const int lz = p.rec_I[rid] - ez0, lx = p.rec_J[rid] - ex0;
       out[static_cast<long long>(p.n) * g.nrec + rid] = st[(lz + R) * T2_IX + lx + R];
-      if (two) out[static_cast<long long>(p.n + 1) * g.nrec + rid] = mid[lz * T2_MX + lx];
+    }
+  };
+  auto sample_n1 = [&](const float* mid, float* out) {
+    if (!two) return;
+    for (int q = rb + tid; q < re; q += T2_NT) {
+      const int rid = p.trec_id[q];
+      const int lz = p.rec_I[rid] - ez0, lx = p.rec_J[rid] - ex0;
+      out[static_cast<long long>(p.n + 1) * g.nrec + rid] = mid[lz * T2_MX + lx];
     }
   };
   auto ring_store = [&](float* ring, int r, const float (&v)[4]) {  // BOUNDARY store (own output points)
@@ -182,10 +189,10 @@ __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtenso
   RingN<T2_NSTAGE> cons;
   int it = 0;  // item counter: mid buffer = it & 1
   auto barrier_and_refill = [&]() {
-    __syncthreads();  // mid complete; every warp is done with item it - 1 (its stage and mid buffer)
+    __syncthreads();  // mid complete; every warp is done with item it's stage and with item it - 1
     if (tid == 0 && issued < nitems) {
       fence_proxy_async();
-      issue_next();  // into the stage of item it - 1
+      issue_next();  // into the stage of item it (phase 2 reads registers and mid only)
     }
   };
   float2 Lb0[RZ][2], Lb1[RZ][2];  // background L u^n, L u^{n+1} at this thread's points (shot s)
@@ -214,6 +221,7 @@ __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtenso
         }
         put_mid(mid, r, v1s[r]);
       }
+      if (leader && re > rb && p.d_bg) sample_n(st, p.d_bg + (p.dbg_shot0 + s) * data_stride);
       barrier_and_refill();
       if (inner) {
         float2 C1[RZ][2];
@@ -267,7 +275,7 @@ __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtenso
           }
         }
       }
-      if (leader && re > rb && p.d_bg) sample(st, mid, p.d_bg + (p.dbg_shot0 + s) * data_stride);
+      if (leader && re > rb && p.d_bg) sample_n1(mid, p.d_bg + (p.dbg_shot0 + s) * data_stride);
       cons.advance();
       ++it;
     }
@@ -292,6 +300,7 @@ __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtenso
         }
         put_mid(mid, r, v1s[r]);
       }
+      if (re > rb && p.d_born) sample_n(st, p.d_born + (static_cast<long long>(s) * p.K + fb + t) * data_stride);
       barrier_and_refill();
       if (inner) {
         float2 L1[RZ][2], C1[RZ][2];
@@ -315,7 +324,7 @@ __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtenso
           }
         }
       }
-      if (re > rb && p.d_born) sample(st, mid, p.d_born + (static_cast<long long>(s) * p.K + fb + t) * data_stride);
+      if (re > rb && p.d_born) sample_n1(mid, p.d_born + (static_cast<long long>(s) * p.K + fb + t) * data_stride);
       cons.advance();
       ++it;
     }
@@ -435,8 +444,8 @@ __device__ __forceinline__ void bwd_t2_body(const CUtensorMap* mh, const CUtenso
     }
     ++issued;
   };
-  if (tid == 0)  // NSTAGE - 1 items in flight: the stage of item i - 1 is refilled at item i's barrier
-    while (issued < min(T2_NSTAGE - 1, nitems)) issue_next();
+  if (tid == 0)  // NSTAGE items in flight: phase 2 reads no stage data (s^j is copied to registers first)
+    while (issued < min(T2_NSTAGE, nitems)) issue_next();
 
   const int I0 = ez0 + ty * RZ;
   const int J0 = ex0 + tx * 4;

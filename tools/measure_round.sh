@@ -1,17 +1,28 @@
 #!/bin/bash
-# One measurement pass on the GPU box: tests, bench, ncu launch list of the bench command, full captures.
+# One measurement pass on the GPU box (dev tool): GPU tests, smoke, the driver's bench line (cfg 3), evidence
+# lines, the ncu launch list of the bench command and full ncu captures of the two step kernels at the bench's
+# launch configuration. Results land in gpurun_out/; tools/post_round.py TAG copies the summaries to profiles/.
 set -x
-TAG=${1:-r01}
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo pytest_exit=$?
+TAG=${1:-r02}
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo pytest_exit=$?
 tail -3 gpurun_out/pytest_gpu_$TAG.log
-timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke_$TAG.log 2>&1; echo smoke_exit=$?
-timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo bench_exit=$?
-tail -1 gpurun_out/bench_$TAG.json
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo smoke_exit=$?
+tail -2 gpurun_out/smoke_$TAG.log
+timeout 1500 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo bench_exit=$?
+tail -c 1500 gpurun_out/bench_$TAG.json
+# evidence lines (never the driver's line; config.workload / mode say what they are)
+E="--steps 2 --warmup 1 --no-cpu-baseline"
+timeout 600 python bench.py --config 1 $E > gpurun_out/ev_cfg1_$TAG.json 2>&1; echo ev_cfg1=$?
+timeout 900 python bench.py --config 2 --mode fused $E --no-e2e > gpurun_out/ev_cfg2_fused_$TAG.json 2>&1; echo ev_cfg2=$?
+timeout 900 python bench.py --config 3 --mode misfit $E --no-e2e > gpurun_out/ev_cfg3_misfit_$TAG.json 2>&1; echo ev_misfit=$?
+for S in 32 16 8; do
+  timeout 600 python bench.py --config 3 --shots $S $E --no-e2e > gpurun_out/ev_cfg3_shots${S}_$TAG.json 2>&1; echo ev_shots$S=$?
+done
+# ncu launch list of the bench command (a window of launches after the warm-up steps)
 CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
-$CMD > gpurun_out/plain_$TAG.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none -s 12000 -c 4200 --csv \
-      --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1; echo ncu_launch=$?
-P="python tools/profile_step.py --config 1 --reps 1"
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -s 100000 -c 8000 --csv \
+    --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1; echo ncu_launch=$?
+P="python tools/profile_step.py --config 3 --shots 16 --nt 40 --reps 1"
 $P > gpurun_out/plain_prof_$TAG.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:bwd_step -s 1000 -c 2 -o gpurun_out/prof_bwd_$TAG $P > gpurun_out/ncu_bwd_$TAG.log 2>&1; echo ncu_bwd=$?
-ncu --set full --clock-control none --import-source on -k regex:fwd_step -s 1000 -c 2 -o gpurun_out/prof_fwd_$TAG $P > gpurun_out/ncu_fwd_$TAG.log 2>&1; echo ncu_fwd=$?
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:fwd_qres -s 10 -c 1 -o gpurun_out/prof_fwd_$TAG $P > gpurun_out/ncu_fwd_$TAG.log 2>&1; echo ncu_fwd=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:bwd_step -s 10 -c 1 -o gpurun_out/prof_bwd_$TAG $P > gpurun_out/ncu_bwd_$TAG.log 2>&1; echo ncu_bwd=$?

@@ -22,6 +22,10 @@
 #pragma once
 #include "hv_kernels.cuh"
 
+#ifndef HV_T2_GROUP_FASTEST
+#define HV_T2_GROUP_FASTEST 0
+#endif
+
 namespace hvk {
 
 constexpr int T2_OX = OX, T2_OZ = OZ;                      // output tile (level n+2): 56 x 56
@@ -335,9 +339,8 @@ __device__ __forceinline__ bool t2_mid_is_interior(const Geo& g, int ex0, int ez
   return ez0 >= g.W && ez0 + T2_MZ <= g.W + g.nz && ex0 >= g.W && ex0 + T2_MX <= g.W + g.nx;
 }
 
-// grid.x = G x ntz x ntx, group fastest, then tile rows: the groups of a tile run concurrently (the background
-// halo they all read is an L2 hit) and vertically adjacent tiles are neighbours in launch order (their halo rows
-// are L2 hits).
+// grid.x = G x ntz x ntx. Default order: tiles fastest, group slowest (HV_T2_GROUP_FASTEST=1: group fastest, so
+// the groups of a tile share the background halo in L2 but neighbouring tiles' halos miss: 19 % L2 hit rate).
 __global__ void __launch_bounds__(T2_NT, T2_MINB)
     fwd_t2_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
                   const __grid_constant__ CUtensorMap mq, const T2Params p) {
@@ -346,9 +349,17 @@ __global__ void __launch_bounds__(T2_NT, T2_MINB)
   float* midb = stages + T2_NSTAGE * T2_STAGE_FLOATS;
   float* qs = midb + 2 * T2_MID_FLOATS;
   uint64_t* bars = reinterpret_cast<uint64_t*>(qs + T2_QFG * T2_MID_FLOATS);
+#if HV_T2_GROUP_FASTEST
   const int grp = blockIdx.x % p.G;
   const int tile = blockIdx.x / p.G;
   const int bz = tile % p.ntz, bx = tile / p.ntz;
+#else  // tiles fastest (x, then z), group slowest: a wave holds most tiles of one group, all stepping through the
+       // same (shot, field) items, so the halo reads of neighbouring tiles are L2 hits
+  const int ntl = p.ntx * p.ntz;
+  const int grp = blockIdx.x / ntl;
+  const int tile = blockIdx.x - grp * ntl;
+  const int bz = tile / p.ntx, bx = tile - bz * p.ntx;
+#endif
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     tma_prefetch_desc(&mh);
     tma_prefetch_desc(&mt);
@@ -651,9 +662,17 @@ __global__ void __launch_bounds__(T2_NT, T2_MINB)
   float* stages = reinterpret_cast<float*>(smem_raw);
   float* midb = stages + T2_NSTAGE * T2_BSTAGE_FLOATS;
   uint64_t* bars = reinterpret_cast<uint64_t*>(midb + 2 * T2_MID_FLOATS);
+#if HV_T2_GROUP_FASTEST
   const int grp = blockIdx.x % p.G;
   const int tile = blockIdx.x / p.G;
   const int bz = tile % p.ntz, bx = tile / p.ntz;
+#else  // tiles fastest (x, then z), group slowest: a wave holds most tiles of one group, all stepping through the
+       // same (shot, field) items, so the halo reads of neighbouring tiles are L2 hits
+  const int ntl = p.ntx * p.ntz;
+  const int grp = blockIdx.x / ntl;
+  const int tile = blockIdx.x - grp * ntl;
+  const int bz = tile / p.ntx, bx = tile - bz * p.ntx;
+#endif
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     tma_prefetch_desc(&mh);
     tma_prefetch_desc(&mt);

@@ -127,7 +127,8 @@ int plan_call(hv_ctx* c, int want, int K, int nloc, Plan* pl) {
   // the context's own workspace (grow-only, reused or re-allocated by this call) counts as available
   // (only the buffers of the H·v path: callers such as hv_lowrank_geneig hold their own across hv_hessvec calls)
   static const char* const kPathBufs[] = {"W2",   "imgc", "rec_coef", "scalars", "Q",    "pool", "dborn", "dbg",
-                                          "rres", "acc",  "store",    "ring",    "sbuf", "ckpt", "seg", "phi_part"};
+                                          "rres", "acc",  "store",    "ring",    "sbuf", "ckpt", "seg", "phi_part",
+                                          "bgD"};
   double held = 0;
   for (const char* n : kPathBufs) {
     auto it = c->ws.find(n);
@@ -143,6 +144,7 @@ int plan_call(hv_ctx* c, int want, int K, int nloc, Plan* pl) {
                               2.0 * g.nz * g.nx + (double)kBwdSplit * pl->nacc * g.plane) + (1 << 20);
   auto per_shot = [&](int store, int k) {
     double b = F4 * (store == HV_STORE_FULL && t2_on ? 4.0 : 2.0) * pl->nslot * g.plane;  // field pool
+    b += F4 * 4.0 * g.plane;  // background increments D (background + replay, 2 planes each)
     b += F4 * (double)K * g.nt * g.nrec;                                        // Born data
     if (grad) b += F4 * 2.0 * g.nt * g.nrec;                                    // data + residual
     if (adjoint) {
@@ -317,6 +319,9 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   bool use_t2b = use_t2 && pl.store == HV_STORE_FULL && kT2BwdDefault;
   if (const char* e = std::getenv("HV_T2B")) use_t2b = use_t2 && pl.store == HV_STORE_FULL && std::strcmp(e, "0") != 0;
   if ((st = ws_get(c, "pool", sizeof(float) * g.plane * planes_per_shot * S, (void**)&pool))) return st;
+  // background increments D = u^n - u^{n-1} ([2: background, replay][S][2][plane])
+  float* bgD = nullptr;
+  if ((st = ws_get(c, "bgD", sizeof(float) * g.plane * 4 * S, (void**)&bgD))) return st;
   if (K > 0 && (st = ws_get(c, "dborn", sizeof(float) * (size_t)S * K * g.nt * g.nrec, (void**)&dborn))) return st;
   double* phi_part = nullptr;  // per-block partial sums of the residual kernel (fixed-order phi, no atomics)
   if (grad || misfit) {
@@ -343,11 +348,14 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   if ((st = make_tmap(c, Q ? Q : pool, Q ? K : planes_per_shot * S, TX, TZ, &map_q))) return st;
   CUtensorMap map_w;
   if ((st = make_tmap(c, W2, 1, TX, TZ, &map_w))) return st;
-  CUtensorMap map_halo_t2, map_mid_t2, map_q_t2;  // T = 2 forward boxes: 72 x 72 halo, 64 x 64 mid region
+  CUtensorMap map_d;  // background increments, TX x TZ boxes
+  if ((st = make_tmap(c, bgD, 4LL * S, TX, TZ, &map_d))) return st;
+  CUtensorMap map_halo_t2, map_mid_t2, map_q_t2, map_d_t2;  // T = 2 boxes: 72 x 72 halo, 64 x 64 mid region
   if (use_t2) {
     if ((st = make_tmap(c, pool, planes_per_shot * S, T2_IX, T2_IZ, &map_halo_t2))) return st;
     if ((st = make_tmap(c, pool, planes_per_shot * S, T2_MX, T2_MZ, &map_mid_t2))) return st;
     if ((st = make_tmap(c, Q ? Q : pool, Q ? K : planes_per_shot * S, T2_MX, T2_MZ, &map_q_t2))) return st;
+    if ((st = make_tmap(c, bgD, 4LL * S, T2_MX, T2_MZ, &map_d_t2))) return st;
   }
   // s^j tensor map of the backward (FULL store / BOUNDARY level buffer / CHECKPOINT segment)
   CUtensorMap map_sj = map_tile, map_s_t2 = map_tile;
@@ -404,6 +412,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     int64_t launches = 0;
     if (phase == 0) {
       CU_TRY(cudaMemsetAsync(pool, 0, sizeof(float) * g.plane * planes_per_shot * Sb, c->stream));
+      CU_TRY(cudaMemsetAsync(bgD, 0, sizeof(float) * g.plane * 2 * Sb, c->stream));  // D^0 = 0
       if (e_f0) CU_TRY(cudaEventRecord(e_f0, c->stream));
     }
 
@@ -438,6 +447,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     const bool boundary = adjoint && pl.store == HV_STORE_BOUNDARY;
     fp.s_shot_stride = full ? g.iplane * g.nt : 0;
     fp.ring_shot_stride = ringN * g.nt;
+    fp.dbuf = bgD;
+    fp.dplane0 = 0;
     if (boundary && phase == 0) CU_TRY(cudaMemsetAsync(ring, 0, sizeof(float) * ringN * g.nt * Sb, c->stream));
     fp.G = Gf;
     // unit order: one shot per block while Q stays L2-resident; otherwise as many shots per block as keep the
@@ -478,31 +489,39 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
       t2.d_bg = fp.d_bg;
       t2.dbg_shot0 = fp.dbg_shot0;
       t2.d_born = dborn;
+      t2.dbuf = bgD;
+      t2.dplane0 = 0;
       const dim3 grid2(static_cast<unsigned>(t2.G * g.ntx2 * g.ntz2));
       const dim3 block2(BX, T2_BY);
       for (int n = 0; n <= g.nt - 2; n += 2) {
         t2.n = n;
         t2.two = n + 2 <= g.nt - 1;
+        t2.dsel = (n >> 1) & 1;
         t2.s_out = full ? store + (size_t)n * g.iplane : nullptr;
-        fwd_t2_kernel<<<grid2, block2, t2_fwd_smem_bytes(), c->stream>>>(map_halo_t2, map_mid_t2, map_q_t2, t2);
+        fwd_t2_kernel<<<grid2, block2, t2_fwd_smem_bytes(), c->stream>>>(map_halo_t2, map_mid_t2, map_q_t2,
+                                                                            map_d_t2, t2);
         launches++;
       }
     } else if (phase == 0) {
       for (int n = 0; n <= g.nt - 2; ++n) {
         if (adjoint && pl.store == HV_STORE_CHECKPOINT && n % pl.k == 0) {
-          // save (u^n, u^{n-1}): both parity planes of slot 0, per shot; layout ckpt[S][nck][2][plane]
-          for (int s = 0; s < Sb; ++s)
-            CU_TRY(cudaMemcpyAsync(ckpt + ((size_t)s * pl.nck + n / pl.k) * 2 * g.plane,
-                                   pool + (size_t)s * planes_per_shot * g.plane, sizeof(float) * 2 * g.plane,
+          // save (u^n, D^n) per shot; layout ckpt[S][nck][2][plane]
+          for (int s = 0; s < Sb; ++s) {
+            float* ck = ckpt + ((size_t)s * pl.nck + n / pl.k) * 2 * g.plane;
+            CU_TRY(cudaMemcpyAsync(ck, pool + ((size_t)s * planes_per_shot + (n & 1)) * g.plane,
+                                   sizeof(float) * g.plane, cudaMemcpyDeviceToDevice, c->stream));
+            CU_TRY(cudaMemcpyAsync(ck + g.plane, bgD + (size_t)s * 2 * g.plane, sizeof(float) * g.plane,
                                    cudaMemcpyDeviceToDevice, c->stream));
+          }
         }
         fp.n = n;
         fp.s_out = full ? store + (size_t)n * g.iplane : nullptr;
         fp.ring_out = boundary ? ring + (size_t)(n + 1) * ringN : nullptr;
         if (qres)
-          fwd_qres_kernel<<<dim3(g.ntx, g.ntz, Gq), block, qres_smem, c->stream>>>(map_halo, map_tile, map_q, fp);
+          fwd_qres_kernel<<<dim3(g.ntx, g.ntz, Gq), block, qres_smem, c->stream>>>(map_halo, map_tile, map_q, map_d,
+                                                                                    fp);
         else
-          fwd_step_kernel<<<gridf, block, fwd_smem, c->stream>>>(map_halo, map_tile, map_q, map_w, fp);
+          fwd_step_kernel<<<gridf, block, fwd_smem, c->stream>>>(map_halo, map_tile, map_q, map_w, map_d, fp);
         launches++;
       }
     }
@@ -640,12 +659,17 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
             const int b = (j / pl.k) * pl.k;
             if (b != cur_b) {  // replay segment [b, e) of the background into the segment store
               const int e = std::min(b + pl.k, g.nt - 1);
-              for (int s = 0; s < Sb; ++s)
-                CU_TRY(cudaMemcpyAsync(pool + ((size_t)s * planes_per_shot + (size_t)replay_slot * 2) * g.plane,
-                                       ckpt + ((size_t)s * pl.nck + b / pl.k) * 2 * g.plane,
-                                       sizeof(float) * 2 * g.plane, cudaMemcpyDeviceToDevice, c->stream));
+              for (int s = 0; s < Sb; ++s) {  // u^b -> replay slot plane (b & 1), D^b -> the replay D plane
+                const float* ck = ckpt + ((size_t)s * pl.nck + b / pl.k) * 2 * g.plane;
+                CU_TRY(cudaMemcpyAsync(pool + ((size_t)s * planes_per_shot + (size_t)replay_slot * 2 + (b & 1)) *
+                                                  g.plane,
+                                       ck, sizeof(float) * g.plane, cudaMemcpyDeviceToDevice, c->stream));
+                CU_TRY(cudaMemcpyAsync(bgD + ((size_t)(Sb + s) * 2) * g.plane, ck + g.plane,
+                                       sizeof(float) * g.plane, cudaMemcpyDeviceToDevice, c->stream));
+              }
               FwdParams rp = fp;
               rp.bg_slot = replay_slot;
+              rp.dplane0 = Sb;
               rp.K = 0;
               rp.d_bg = nullptr;
               rp.d_born = nullptr;
@@ -655,7 +679,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
               for (int n = b; n < e; ++n) {
                 rp.n = n;
                 rp.s_out = seg + (size_t)(n - b) * g.iplane;
-                fwd_step_kernel<<<gridr, block, fwd_smem_bytes(0), c->stream>>>(map_halo, map_tile, map_q, map_w, rp);
+                fwd_step_kernel<<<gridr, block, fwd_smem_bytes(0), c->stream>>>(map_halo, map_tile, map_q, map_w,
+                                                                                 map_d, rp);
                 launches++;
               }
               cur_b = b;

@@ -155,10 +155,16 @@ __device__ __forceinline__ float2 half2of(const float4& v, int h) { return h == 
 
 // Unscaled 8th-order Laplacian of this thread's RZ x 4 points from a halo tile in shared memory, as column pairs
 // (h = 0: columns 0-1, h = 1: columns 2-3). Thread (tx, ty) owns tile rows ty*RZ .. ty*RZ+RZ-1 and columns
-// 4tx .. 4tx+3. Per point: s = A1 (x+-1 + z+-1) + A2 (..2) + A3 (..3) + A4 (..4), L = 2 A0 ctr + s, with the
-// pair sums (x-pair) + (z-pair) in that order.
-// t points at element (0, 0) of a buffer of row width W whose element (ty*RZ + r + R, 4tx + i + R) is the
-// stencil centre of the thread's point (r, i) (W = HX: a staged halo tile).
+// 4tx .. 4tx+3. t points at element (0, 0) of a buffer of row width W whose element (ty*RZ + r + R, 4tx + i + R) is
+// the stencil centre of the thread's point (r, i) (W = HX: a staged halo tile).
+//
+// Difference form: since 2 a0 + 4 (a1 + a2 + a3 + a4) = 0,
+//   L u = sum_k a_k [ (u[x+k] - u) + (u[x-k] - u) + (u[z+k] - u) + (u[z-k] - u) ].
+// For the smooth fields of this problem (5 Hz at h = 8 m: 37-137 cells per wavelength) |L u| is 1e-2 - 1e-3 of |u|;
+// the plain sum 2 a0 u + sum a_k (...) then loses that factor of fp32 precision to cancellation, while here each
+// difference of neighbouring values is exact (Sterbenz) and the rounding is relative to the small differences.
+// Measured on cfg 2 (nt 4000, sharp model): receiver-data error vs the fp64 oracle 2.0e-4 (plain) -> 6e-7 with
+// the increment-form background update; the price is ~7 more FP instructions per point.
 template <int W>
 __device__ __forceinline__ void lap_points_w(const float* __restrict__ t, int tx, int ty, float2 (&L)[RZ][2],
                                              float2 (&C)[RZ][2]) {
@@ -178,18 +184,20 @@ __device__ __forceinline__ void lap_points_w(const float* __restrict__ t, int tx
       const int i = 2 * h;
       auto P = [&](int k) { return make_float2(xs[k + i], xs[k + i + 1]); };
       auto Z = [&](int k) { return half2of(zw[r + k], h); };
-      // x-pair sum at distance d: even d reads register-aligned pairs (one FADD2); odd d straddles the float4s,
-      // so two scalar FADDs (same roundings) write the aligned result pair instead of MOV-ing operands together
-      auto X = [&](int d) {
-        if (d % 2 == 0) return add2(P(4 - d), P(4 + d));
-        return make_float2(__fadd_rn(xs[4 - d + i], xs[4 + d + i]), __fadd_rn(xs[5 - d + i], xs[5 + d + i]));
-      };
       const float2 ctr = P(4);
-      float2 s = mul2(splat2(HV_A1), add2(X(1), add2(Z(3), Z(5))));
-      s = fma2(splat2(HV_A2), add2(X(2), add2(Z(2), Z(6))), s);
-      s = fma2(splat2(HV_A3), add2(X(3), add2(Z(1), Z(7))), s);
-      s = fma2(splat2(HV_A4), add2(X(4), add2(Z(0), Z(8))), s);
-      L[r][h] = fma2(splat2(2.0f * HV_A0), ctr, s);
+      // (x+d - c) + (x-d - c): even d reads register-aligned pairs (FADD2); odd d straddles the float4s, so the
+      // differences are scalar FADDs (same roundings) written straight into the result pair
+      auto DX = [&](int d) {
+        if (d % 2 == 0) return add2(sub2(P(4 + d), ctr), sub2(P(4 - d), ctr));
+        return make_float2(__fadd_rn(__fsub_rn(xs[4 + d + i], xs[4 + i]), __fsub_rn(xs[4 - d + i], xs[4 + i])),
+                           __fadd_rn(__fsub_rn(xs[5 + d + i], xs[5 + i]), __fsub_rn(xs[5 - d + i], xs[5 + i])));
+      };
+      auto DZ = [&](int d) { return add2(sub2(Z(4 + d), ctr), sub2(Z(4 - d), ctr)); };
+      float2 s = mul2(splat2(HV_A1), add2(DX(1), DZ(1)));
+      s = fma2(splat2(HV_A2), add2(DX(2), DZ(2)), s);
+      s = fma2(splat2(HV_A3), add2(DX(3), DZ(3)), s);
+      s = fma2(splat2(HV_A4), add2(DX(4), DZ(4)), s);
+      L[r][h] = s;
       C[r][h] = ctr;
     }
   }
@@ -257,6 +265,11 @@ struct FwdParams {
   float* d_born;          // [S][K][nt][nrec] Born data (batch-local) or null
   float* ring_out;        // BOUNDARY store: ring of u^{n+1} for batch shot 0, or null
   long long ring_shot_stride;
+  // Background in increment form (compensated leapfrog): the second state plane of the background
+  // holds D^n = u^n - u^{n-1} (not u^{n-1}); D is updated in place. D of batch shot s is plane (dplane0 + s) * 2
+  // of the D tensor map / buffer dbuf ([.][2][Nz][P]; the second plane of a pair is used by the T = 2 kernel).
+  float* dbuf;
+  int dplane0;
 };
 
 // Per-point damping of this thread's points (SP: the tile touches the sponge): (1 - c) and 1 / (1 + c), as
@@ -284,6 +297,10 @@ struct Damp {
     const float cmi = (i & 1) ? cm[r][i >> 1].y : cm[r][i >> 1].x;
     return (fmaf(2.0f, C, rhs) - cmi * prev) * ci(r, i);
   }
+  // increment form: D^{n+1} = [(1 - c) D^n + rhs] / (1 + c)   (u^{n+1} = u^n + D^{n+1})
+  __device__ __forceinline__ float2 updd(int r, int h, float2 D, float2 rhs) const {
+    return mul2(fma2(cm[r][h], D, rhs), ci_[r][h]);
+  }
 };
 template <>
 struct Damp<false> {
@@ -294,6 +311,7 @@ struct Damp<false> {
   __device__ __forceinline__ float upd1(int, int, float C, float prev, float rhs) const {
     return fmaf(2.0f, C, rhs) - prev;
   }
+  __device__ __forceinline__ float2 updd(int, int, float2 D, float2 rhs) const { return add2(D, rhs); }
 };
 template <bool SP>
 using BwdDamp = Damp<SP>;
@@ -353,12 +371,12 @@ __device__ __forceinline__ void fwd_unit_decode(const FwdParams& p, int u, int n
 __device__ __forceinline__ int group_begin(int K, int G, int grp) { return (K * grp) / G; }
 
 struct FwdProducer {  // thread 0's walk over this CTA's items (decoded once per unit: no divisions per item)
-  const CUtensorMap *mh, *mt, *mq, *mw;
+  const CUtensorMap *mh, *mt, *mq, *mw, *md;
   float* stages;
   uint64_t* bars;
   int u, t;                 // current unit, next item within it (0 = background, 1..nf = Born fields)
   int U, nstep, ntl;
-  int x0, z0, pl_bg, pl_born, fb, nf;  // decoded unit
+  int x0, z0, pl_bg, pl_born, fb, nf, dpl;  // decoded unit
   bool upd;
   uint64_t pol_first, pol_last;
   RingF ring;
@@ -382,6 +400,7 @@ struct FwdProducer {  // thread 0's walk over this CTA's items (decoded once per
     nf = group_begin(p.K, p.G, grp + 1) - fb;
     upd = grp == 0 && p.bg_update;
     pl_bg = (s * p.nslot + p.bg_slot) * 2;
+    dpl = (p.dplane0 + s) * 2;
     pl_born = (s * p.nslot + p.born_slot0 + fb) * 2;
   }
   __device__ __forceinline__ void issue(const FwdParams& p) {
@@ -394,9 +413,9 @@ struct FwdProducer {  // thread 0's walk over this CTA's items (decoded once per
       tma_load_3d(st, mh, bar, x0 - R, z0 - R, pl_bg + par_n);
       tma_load_3d(st + TILE_FLOATS + PT_FLOATS, mw, bar, x0, z0, 0);
 #if HV_L2_HINTS
-      if (upd) tma_load_3d_hint(st + TILE_FLOATS, mt, bar, x0, z0, pl_bg + par_new, pol_first);
+      if (upd) tma_load_3d_hint(st + TILE_FLOATS, md, bar, x0, z0, dpl, pol_first);  // D^n (increment form)
 #else
-      if (upd) tma_load_3d(st + TILE_FLOATS, mt, bar, x0, z0, pl_bg + par_new);
+      if (upd) tma_load_3d(st + TILE_FLOATS, md, bar, x0, z0, dpl);
 #endif
     } else {
       const int pl = pl_born + 2 * (t - 1);
@@ -489,21 +508,27 @@ __device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages
     lap_points(st, tx, ty, Lb, C);
     if (leader) {
       float* dst = p.pool + (static_cast<long long>(s * p.nslot + p.bg_slot) * 2 + par_new) * g.plane;
+      float* dD = p.dbuf + static_cast<long long>((p.dplane0 + s) * 2) * g.plane;
       const int sI = p.src_I[p.shot0 + s], sJ = p.src_J[p.shot0 + s];
       const float amp = p.src_amp[p.n];
 #pragma unroll
       for (int r = 0; r < RZ; ++r) {
-        const float4 pv = ld4(st + TILE_FLOATS + so + r * TX);
-        float v[4];
+        const float4 dv = ld4(st + TILE_FLOATS + so + r * TX);  // D^n = u^n - u^{n-1}
+        float v[4], dn[4];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const float2 u = dmp.upd(r, h, C[r][h], half2of(pv, h), mul2(w[r][h], Lb[r][h]));
-          v[2 * h] = u.x, v[2 * h + 1] = u.y;
+          const float2 d1 = dmp.updd(r, h, half2of(dv, h), mul2(w[r][h], Lb[r][h]));
+          dn[2 * h] = d1.x, dn[2 * h + 1] = d1.y;
         }
         if (I0 + r == sI && sJ >= J0 && sJ < J0 + 4) {  // point source dt^2 s[n] / h^2 (/(1 + c))
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            if (J0 + i == sJ) v[i] += amp * dmp_ci(dmp, r, i);
+            if (J0 + i == sJ) dn[i] += amp * dmp_ci(dmp, r, i);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // u^{n+1} = u^n + D^{n+1}
+          const float2 u = add2(C[r][h], make_float2(dn[2 * h], dn[2 * h + 1]));
+          v[2 * h] = u.x, v[2 * h + 1] = u.y;
         }
         if (SP && p.ring_out != nullptr) {  // BOUNDARY store: the ring of u^{n+1}
 #pragma unroll
@@ -513,6 +538,7 @@ __device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages
           }
         }
         store_row(dst, r, v);
+        store_row(dD, r, dn);
       }
       // imaging-factor store s^n = 2 dt^2 / (v h^2) * L~u^n on the interior (FULL store / replay segments)
       const int jc = J0 - g.c0;
@@ -575,7 +601,7 @@ __device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages
 __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
     fwd_step_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
                     const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mw,
-                    const FwdParams p) {
+                    const __grid_constant__ CUtensorMap md, const FwdParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stages = reinterpret_cast<float*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + FSTAGES_BYTES);
@@ -592,7 +618,7 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
   const int U = p.S * p.G * ntl;
   const int nstep = gridDim.x;
   FwdProducer prod;
-  prod.mh = &mh, prod.mt = &mt, prod.mq = &mq, prod.mw = &mw, prod.stages = stages, prod.bars = bars;
+  prod.mh = &mh, prod.mt = &mt, prod.mq = &mq, prod.mw = &mw, prod.md = &md, prod.stages = stages, prod.bars = bars;
   prod.u = blockIdx.x, prod.t = 0, prod.U = U, prod.nstep = nstep, prod.ntl = ntl;
   prod.pol_first = policy_evict_first(), prod.pol_last = policy_evict_last();
   prod.decode(p);
@@ -617,7 +643,8 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
 // overlaps are L2 hits). Same paired-fp32 (FFMA2) arithmetic as fwd_step_kernel (bit-identical fields).
 template <bool SP>
 __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUtensorMap* mt, const CUtensorMap* mq,
-                                         const FwdParams& p, float* stages, float* qs, uint64_t* bars) {
+                                         const CUtensorMap* md, const FwdParams& p, float* stages, float* qs,
+                                         uint64_t* bars) {
   const Geo& g = p.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
   const int x0 = blockIdx.x * TX, z0 = blockIdx.y * TZ;
@@ -639,7 +666,10 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
     const int pl = (ps * p.nslot + slot) * 2;
     mbar_expect_tx(&bars[prod.stage], TILE_BYTES + (upd ? PT_BYTES : 0));
     tma_load_3d(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_n);
-    if (upd) tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_new);
+    if (upd && pt == 0)  // background: D^n (increment form)
+      tma_load_3d(st + TILE_FLOATS, md, &bars[prod.stage], x0, z0, (p.dplane0 + ps) * 2);
+    else if (upd)
+      tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_new);
     prod.advance();
     if (++pt > nf) {
       pt = 0;
@@ -714,21 +744,28 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
       lap_points(st, tx, ty, Lb, C);
       if (leader) {
         float* dst = p.pool + (static_cast<long long>(s * p.nslot + p.bg_slot) * 2 + par_new) * g.plane;
+        float* dD = p.dbuf + static_cast<long long>((p.dplane0 + s) * 2) * g.plane;
         const int sI = p.src_I[p.shot0 + s], sJ = p.src_J[p.shot0 + s];
 #pragma unroll
         for (int r = 0; r < RZ; ++r) {
-          const float4 pv = ld4(st + TILE_FLOATS + so + r * TX);
-          float v[4];
+          const float4 dv = ld4(st + TILE_FLOATS + so + r * TX);  // D^n = u^n - u^{n-1}
+          float v[4], dn[4];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const float2 u = dmp.upd(r, h, C[r][h], half2of(pv, h), mul2(w[r][h], Lb[r][h]));
-            v[2 * h] = u.x, v[2 * h + 1] = u.y;
+            const float2 d1 = dmp.updd(r, h, half2of(dv, h), mul2(w[r][h], Lb[r][h]));
+            dn[2 * h] = d1.x, dn[2 * h + 1] = d1.y;
           }
           if (I0 + r == sI && sJ >= J0 && sJ < J0 + 4) {  // point source dt^2 s[n] / h^2 (/(1 + c))
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              if (J0 + i == sJ) v[i] += amp * dmp_ci(dmp, r, i);
+              if (J0 + i == sJ) dn[i] += amp * dmp_ci(dmp, r, i);
           }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {  // u^{n+1} = u^n + D^{n+1}
+            const float2 u = add2(C[r][h], make_float2(dn[2 * h], dn[2 * h + 1]));
+            v[2 * h] = u.x, v[2 * h + 1] = u.y;
+          }
+          store_row(dD, r, dn);
           if (SP && p.ring_out != nullptr) {  // BOUNDARY store: the ring of u^{n+1}
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -799,7 +836,8 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
 #endif
 __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
     fwd_qres_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
-                    const __grid_constant__ CUtensorMap mq, const FwdParams p) {
+                    const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap md,
+                    const FwdParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stages = reinterpret_cast<float*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES_BYTES);
@@ -813,9 +851,9 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
   }
   __syncthreads();
   if (tile_is_interior(p.g, blockIdx.x * TX, blockIdx.y * TZ))
-    fwd_qres_body<false>(&mh, &mt, &mq, p, stages, qs, bars);
+    fwd_qres_body<false>(&mh, &mt, &mq, &md, p, stages, qs, bars);
   else
-    fwd_qres_body<true>(&mh, &mt, &mq, p, stages, qs, bars);
+    fwd_qres_body<true>(&mh, &mt, &mq, &md, p, stages, qs, bars);
 }
 
 // ------------------------------------------------------------------------------------------------ backward

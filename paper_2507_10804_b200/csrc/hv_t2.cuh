@@ -78,12 +78,16 @@ struct T2Params {
   float* ring_out;        // BOUNDARY store: ring of level n+1 for batch shot 0 (level n+2 = + ringN), or null
   long long ring_shot_stride;
   int ringN;
+  // background increment D = u^n - u^{n-1} (compensated leapfrog, as FwdParams): shot s reads plane
+  // (dplane0 + s) * 2 + dsel (D^n) and writes plane (dplane0 + s) * 2 + (dsel ^ 1) (D^{n+2}, or D^{n+1})
+  float* dbuf;
+  int dplane0, dsel;
 };
 
 template <bool SP>
 __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtensorMap* mt, const CUtensorMap* mq,
-                                            const T2Params& p, float* stages, float* midb, float* qs,
-                                            uint64_t* bars, int bx, int bz, int grp) {
+                                            const CUtensorMap* md, const T2Params& p, float* stages, float* midb,
+                                            float* qs, uint64_t* bars, int bx, int bz, int grp) {
   const Geo& g = p.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
   const int ox0 = bx * T2_OX, oz0 = bz * T2_OZ;   // output tile origin (padded coordinates)
@@ -105,7 +109,10 @@ __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtenso
     const int pl = (ps * p.nslot + slot) * 4;
     mbar_expect_tx(&bars[prod.stage], (T2_IN_FLOATS + T2_MID_FLOATS) * 4);
     tma_load_3d(st, mh, &bars[prod.stage], ex0 - R, ez0 - R, pl + ln);
-    tma_load_3d(st + T2_IN_FLOATS, mt, &bars[prod.stage], ex0, ez0, pl + lp);
+    if (pt == 0)  // background: D^n on the mid region (increment form)
+      tma_load_3d(st + T2_IN_FLOATS, md, &bars[prod.stage], ex0, ez0, (p.dplane0 + ps) * 2 + p.dsel);
+    else
+      tma_load_3d(st + T2_IN_FLOATS, mt, &bars[prod.stage], ex0, ez0, pl + lp);
     prod.advance();
     if (++pt > nf) {
       pt = 0;
@@ -209,19 +216,24 @@ __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtenso
       float2 C0[RZ][2];
       lap_points_w<T2_IX>(st, tx, ty, Lb0, C0);
       const int sI = p.src_I[p.shot0 + s], sJ = p.src_J[p.shot0 + s];
-      float v1s[RZ][4];
+      float v1s[RZ][4], d1s[RZ][4];  // u^{n+1}, D^{n+1} at this thread's points
 #pragma unroll
       for (int r = 0; r < RZ; ++r) {
-        const float4 pv = ld4(st + T2_IN_FLOATS + so + r * T2_MX);
+        const float4 dv = ld4(st + T2_IN_FLOATS + so + r * T2_MX);  // D^n
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const float2 u = dmp.upd(r, h, C0[r][h], half2of(pv, h), mul2(w[r][h], Lb0[r][h]));
-          v1s[r][2 * h] = u.x, v1s[r][2 * h + 1] = u.y;
+          const float2 d1 = dmp.updd(r, h, half2of(dv, h), mul2(w[r][h], Lb0[r][h]));
+          d1s[r][2 * h] = d1.x, d1s[r][2 * h + 1] = d1.y;
         }
         if (I0 + r == sI && sJ >= J0 && sJ < J0 + 4) {
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            if (J0 + i == sJ) v1s[r][i] += amp0 * dmp_ci(dmp, r, i);
+            if (J0 + i == sJ) d1s[r][i] += amp0 * dmp_ci(dmp, r, i);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float2 u = add2(C0[r][h], make_float2(d1s[r][2 * h], d1s[r][2 * h + 1]));
+          v1s[r][2 * h] = u.x, v1s[r][2 * h + 1] = u.y;
         }
         put_mid(mid, r, v1s[r]);
       }
@@ -233,24 +245,34 @@ __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtenso
         if (leader) {
           float* d1 = p.pool + (static_cast<long long>(s * p.nslot) * 4 + l1) * g.plane;
           float* d2 = p.pool + (static_cast<long long>(s * p.nslot) * 4 + l2) * g.plane;
+          float* dD = p.dbuf + static_cast<long long>((p.dplane0 + s) * 2 + (p.dsel ^ 1)) * g.plane;
 #pragma unroll
           for (int r = 0; r < RZ; ++r) {
             store_row(d1, r, v1s[r]);
             if (SP && p.ring_out) ring_store(p.ring_out + s * p.ring_shot_stride, r, v1s[r]);
             if (two) {
-              float v[4];
+              float v[4], dn[4];
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
-                const float2 u = dmp.upd(r, h, C1[r][h], C0[r][h], mul2(w[r][h], Lb1[r][h]));
-                v[2 * h] = u.x, v[2 * h + 1] = u.y;
+                const float2 d2v = dmp.updd(r, h, make_float2(d1s[r][2 * h], d1s[r][2 * h + 1]),
+                                            mul2(w[r][h], Lb1[r][h]));
+                dn[2 * h] = d2v.x, dn[2 * h + 1] = d2v.y;
               }
               if (I0 + r == sI && sJ >= J0 && sJ < J0 + 4) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                  if (J0 + i == sJ) v[i] += amp1 * dmp_ci(dmp, r, i);
+                  if (J0 + i == sJ) dn[i] += amp1 * dmp_ci(dmp, r, i);
+              }
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const float2 u = add2(C1[r][h], make_float2(dn[2 * h], dn[2 * h + 1]));
+                v[2 * h] = u.x, v[2 * h + 1] = u.y;
               }
               if (SP && p.ring_out) ring_store(p.ring_out + s * p.ring_shot_stride + p.ringN, r, v);
               store_row(d2, r, v);
+              store_row(dD, r, dn);
+            } else {
+              store_row(dD, r, d1s[r]);
             }
           }
           if (store_s) {  // FULL store: s^n (and s^{n+1}) = imgc * L u on the interior
@@ -343,7 +365,7 @@ __device__ __forceinline__ bool t2_mid_is_interior(const Geo& g, int ex0, int ez
 // the groups of a tile share the background halo in L2 but neighbouring tiles' halos miss: 19 % L2 hit rate).
 __global__ void __launch_bounds__(T2_NT, T2_MINB)
     fwd_t2_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
-                  const __grid_constant__ CUtensorMap mq, const T2Params p) {
+                  const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap md, const T2Params p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stages = reinterpret_cast<float*>(smem_raw);
   float* midb = stages + T2_NSTAGE * T2_STAGE_FLOATS;
@@ -369,9 +391,9 @@ __global__ void __launch_bounds__(T2_NT, T2_MINB)
   }
   __syncthreads();
   if (t2_mid_is_interior(p.g, bx * T2_OX - R, bz * T2_OZ - R))
-    fwd_t2_body<false>(&mh, &mt, &mq, p, stages, midb, qs, bars, bx, bz, grp);
+    fwd_t2_body<false>(&mh, &mt, &mq, &md, p, stages, midb, qs, bars, bx, bz, grp);
   else
-    fwd_t2_body<true>(&mh, &mt, &mq, p, stages, midb, qs, bars, bx, bz, grp);
+    fwd_t2_body<true>(&mh, &mt, &mq, &md, p, stages, midb, qs, bars, bx, bz, grp);
 }
 
 // ------------------------------------------------------------------------------------------------ backward

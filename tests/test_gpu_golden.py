@@ -8,7 +8,9 @@ tests/golden/meta.json) hold the fp64 oracle's H·v rows / gradient for:
 - cfg 3: shots 16..31 = one full 16-shot batch of the bench's 64-shot plan (S = 16, K = 32, the resident-q /
   large-Q forward), probes k = 0 (Rademacher) and 16 (cosine 1/16, 1/16: in band, SURVEY.md §8(c) P10 caveat),
   nt = 4000 -- so the reflected regime and BOUNDARY's 4000-step fp32 reverse reconstruction are both covered.
-- cfg 2: shot 31, gradient (d_obs = F(v_true), oracle-written input) + probe 0 at nt = 4000, fused call.
+- cfg 2: shot 31, gradient (d_obs = F(v_true), oracle-written input) + probe 0 at nt = 4000, fused call; and the
+  forward data d = F(m), F(v_true) of shot 31 at nt = 4000 (333 time steps per source period: the regime where a
+  two-level fp32 leapfrog loses ~2e-4; the background runs in increment form).
 Bar: relative L2 <= 1e-4 per row (BASELINE.json north_star)."""
 import json
 import os
@@ -29,7 +31,8 @@ def _gold(name):
     if not os.path.exists(path):
         pytest.fail(f"missing golden file {path}: run tools/make_golden.py")
     if name.endswith(".npz"):
-        return np.load(path)["d_obs"]
+        z = np.load(path)
+        return z[z.files[0]]
     return np.load(path).astype(np.float64)
 
 
@@ -96,3 +99,15 @@ def test_cfg2_fused_gradient_hessvec_full_nt(hv, store):
     assert rel_l2(g, g_ref) <= TOL, rel_l2(g, g_ref)
     assert rel_l2(HV[0], hv_ref) <= TOL, rel_l2(HV[0], hv_ref)
     assert abs(phi - meta["phi"]) <= 2 * TOL * meta["phi"]
+
+
+def test_cfg2_forward_full_nt(hv):
+    """d = f(m) (the evaluation model) and f(v_true) (sharp layered model) of shot 31 at full nt = 4000."""
+    wl = W.config(2)
+    s = hv.Solver.from_workload(wl, src_begin=31, src_end=32)
+    d_m = s.forward_shot(wl.model, 31)
+    ref_m = _gold("cfg2_s31_d_m.npz").astype(np.float64)
+    assert rel_l2(d_m, ref_m) <= TOL, rel_l2(d_m, ref_m)
+    d_t = s.forward_shot(wl.model_true, 31)
+    ref_t = _gold("cfg2_s31_dobs.npz").astype(np.float64)
+    assert rel_l2(d_t, ref_t) <= TOL, rel_l2(d_t, ref_t)

@@ -172,10 +172,10 @@ def test_deterministic_and_batch_invariant(hv, ragged):
 
 @pytest.mark.parametrize("nt,K", [(300, 3), (301, 7), (161, 9)])
 def test_t2_kernels_match_single_step(hv, nt, K, monkeypatch):
-    """The T = 2 forward (fwd_t2_kernel: two levels per launch, resident q_k, groups of <= 4 Born fields)
-    computes every level with the single-step kernels' exact per-point operations: d, the FULL store, and hence
-    g, phi and H·v are bitwise identical with HV_T2=0. Even and odd numbers of steps (nt - 1: a trailing
-    one-level launch), one and several Born-field groups; and against the oracle."""
+    """The T = 2 forward (fwd_t2_kernel: two levels per launch, resident q_k, groups of <= 4 Born fields) and
+    adjoint (bwd_t2_kernel) compute every level with the single-step kernels' per-point operations: d, g, phi and
+    H·v agree with HV_T2=0 to rounding. Even and odd numbers of steps (nt - 1: a trailing one-level launch), one
+    and several Born-field groups; and against the oracle."""
     wl = W.custom(70, 150, nt=nt, ns=3, nrec=37, n_probes=K, f_peak=15.0, seed=5)
     V = wl.probes()
     d_obs = np.zeros((wl.ns, wl.nt, wl.nrec), np.float32)
@@ -188,11 +188,13 @@ def test_t2_kernels_match_single_step(hv, nt, K, monkeypatch):
         assert s.stats()["fwd_kernel"] == (3 if t2 == "1" else 0)
         assert s.stats()["bwd_kernel"] == (3 if t2b == "1" else 0)
     (d1, (p1, g1), h1), (d0, (p0, g0), h0) = out["10"], out["00"]
-    assert np.array_equal(d1, d0)
-    assert p1 == p0 and np.array_equal(g1, g0) and np.array_equal(h1, h0)
-    # T = 2 adjoint: lambda levels bit-identical, imaging summed two levels per launch (fp32 summation order)
+    # same per-point operations; since the background runs in increment form the T = 2 and single-step paths
+    # differ by isolated 1-ulp roundings at the wavefront (measured 6e-8 relative), so: rounding-level agreement
+    assert rel_l2(d1, d0) <= 1e-6 and abs(p1 - p0) <= 1e-6 * p0
+    assert rel_l2(g1, g0) <= 1e-6 and rel_l2(h1, h0) <= 1e-6
+    # T = 2 adjoint: imaging summed two levels per launch (fp32 summation order)
     d2, (p2, g2), h2 = out["11"]
-    assert np.array_equal(d2, d0) and p2 == p0
+    assert np.array_equal(d2, d1) and p2 == p1
     assert rel_l2(g2, g0) <= 1e-6 and rel_l2(h2, h0) <= 1e-6
     ref = wave.Problem(wl).hessvec(list(V.astype(np.float64)))
     assert rel_l2(h1, ref) <= TOL and rel_l2(h2, ref) <= TOL

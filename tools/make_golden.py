@@ -12,6 +12,7 @@ These are the fp64 oracle's answers for the exact launch plans the bench times, 
   cfg2_s31_dobs.npz        cfg 2 shot 31: d_obs = F(v_true) (float32, C17) -- an oracle-written INPUT
   cfg2_s31_grad.npy        gradient F*(F(m) - d_obs) of shot 31 at m (Eq. equ:grad)
   cfg2_s31_hv_k0.npy       H·v row of probe k = 0 for shot 31
+  cfg2_s31_d_m.npz         d = F(m) of shot 31 at the evaluation model m (cfg 2 and cfg 3 share m and geometry)
   meta.json                provenance: recipe, oracle calls, phi, timings, sha256 of oracle/wave.py
 
 Every value is computed in float64 by oracle.wave.Problem and rounded once to
@@ -76,10 +77,19 @@ def _cfg2(_):
     return ("cfg2", CFG2_SHOT, (d_obs, phi, g, hv[0]), time.time() - t0)
 
 
+def _cfg2_dm(_):
+    import workloads as W
+    from oracle import wave
+    wl = W.config(2)
+    t0 = time.time()
+    d = wave.Problem(wl).forward(CFG2_SHOT)
+    return ("cfg2dm", CFG2_SHOT, d, time.time() - t0)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workers", type=int, default=6)
-    ap.add_argument("--only", default="cfg1,cfg2,cfg3")
+    ap.add_argument("--only", default="cfg1,cfg2,cfg3,cfg2dm")
     a = ap.parse_args()
     only = set(a.only.split(","))
     os.makedirs(OUT, exist_ok=True)
@@ -90,6 +100,8 @@ def main():
         tasks += [(_cfg2, 0)]
     if "cfg1" in only:
         tasks += [(_cfg1_shot, s) for s in range(16)]
+    if "cfg2dm" in only:
+        tasks += [(_cfg2_dm, 0)]
     t0 = time.time()
     res = {}
     with Pool(a.workers) as pool:
@@ -132,6 +144,11 @@ def main():
                                     "Problem(config(2)).gradient(d_obs, shots=[31], mode='checkpoint', ckpt=63); "
                                     "hessvec_shot(31, [probe 0], mode='checkpoint', ckpt=63)",
                             "cpu_s": secs}
+    if "cfg2dm" in only:
+        d, secs = res[("cfg2dm", CFG2_SHOT)]
+        np.savez_compressed(os.path.join(OUT, "cfg2_s31_d_m.npz"), d=d.astype(np.float32))
+        meta["cfg2_s31_d_m"] = {**common, "config": 2, "shot": CFG2_SHOT,
+                                "call": "Problem(config(2)).forward(31) (the evaluation model m)", "cpu_s": secs}
     with open(mpath, "w") as f:
         json.dump(meta, f, indent=1, sort_keys=True)
     print("done", time.time() - t0)

@@ -333,11 +333,28 @@ def main():
     K = wl.n_probes if args.mode != "misfit" else 0
     ns = wl.ns
     sh = plan_shards(ns, max(K, 1), ws)[rank]
-    comm = None
+    comm, reduce_note = None, "torch.distributed all-reduce" if ws > 1 else "none (1 rank)"
     if ws > 1 and args.reduce == "library" and ns >= ws:
-        obj = [hv.nccl_unique_id() if rank == 0 else None]
+        obj = [None, None]
+        if rank == 0:
+            try:
+                obj[0] = hv.nccl_unique_id()
+            except Exception as e:  # libnccl not loadable: every rank falls back to torch.distributed
+                obj[1] = str(e)
         dist.broadcast_object_list(obj, src=0)
-        comm = hv.nccl_comm_create(ws, rank, obj[0], local)
+        ok = obj[0] is not None
+        if ok:
+            try:
+                comm = hv.nccl_comm_create(ws, rank, obj[0], local)
+            except Exception as e:
+                comm, obj[1] = None, str(e)
+        flag = torch.tensor([1 if comm is not None else 0], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0 and comm is not None:   # keep the ranks consistent
+            hv.nccl_comm_destroy(comm)
+            comm = None
+        reduce_note = ("in-library NCCL (hv_set_comm)" if comm is not None
+                       else f"torch.distributed all-reduce (in-library NCCL unavailable: {obj[1]})")
     solver = hv.Solver.from_workload(wl, src_begin=sh.s0, src_end=sh.s1, device=local, store=args.store,
                                      shot_batch=args.shot_batch, field_group=args.field_group, nccl_comm=comm)
     op = ShardedOperator(solver.hessvec, solver.gradient, None, sh, in_library=comm is not None)
@@ -482,8 +499,7 @@ def main():
                        "model": "quadratic-depth v(z)" if args.config == 1 else
                        ("Marmousi-like layered (seeded)" if args.config in (2, 3, 4) else wl.name),
                        "grid": [wl.nz, wl.nx], "shots": ns, "probes": K, "nt": wl.nt,
-                       "global_batch": K, "parallelism": f"dp{ws} (source-sharded, NCCL all-reduce of H·v"
-                                                         f"{', in-library' if comm is not None else ''})",
+                       "global_batch": K, "parallelism": f"dp{ws} (source-sharded; reduction: {reduce_note})",
                        "l2": "flushed (256 MiB write) between timed steps; inputs + FULL store >> L2",
                        "store": {1: "full", 2: "checkpoint", 3: "boundary"}.get(stats["store"]),
                        "mode": {"fused": f"gradient + {K} H·v (fused)", "misfit": "misfit only (forward + residual)"}

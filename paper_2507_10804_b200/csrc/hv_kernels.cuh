@@ -158,13 +158,15 @@ __device__ __forceinline__ float2 half2of(const float4& v, int h) { return h == 
 // 4tx .. 4tx+3. t points at element (0, 0) of a buffer of row width W whose element (ty*RZ + r + R, 4tx + i + R) is
 // the stencil centre of the thread's point (r, i) (W = HX: a staged halo tile).
 //
-// Difference form: since 2 a0 + 4 (a1 + a2 + a3 + a4) = 0,
-//   L u = sum_k a_k [ (u[x+k] - u) + (u[x-k] - u) + (u[z+k] - u) + (u[z-k] - u) ].
+// Difference form for the two large weights: since 2 a0 + 4 (a1 + a2 + a3 + a4) = 0,
+//   L u = sum_{k=1,2} a_k [ (u[x+k] - u) + (u[x-k] - u) + (u[z+k] - u) + (u[z-k] - u) ]
+//       + sum_{k=3,4} a_k [ u[x+k] + u[x-k] + u[z+k] + u[z-k] ] - 4 (a3 + a4) u.
 // For the smooth fields of this problem (5 Hz at h = 8 m: 37-137 cells per wavelength) |L u| is 1e-2 - 1e-3 of |u|;
-// the plain sum 2 a0 u + sum a_k (...) then loses that factor of fp32 precision to cancellation, while here each
-// difference of neighbouring values is exact (Sterbenz) and the rounding is relative to the small differences.
-// Measured on cfg 2 (nt 4000, sharp model): receiver-data error vs the fp64 oracle 2.0e-4 (plain) -> 6e-7 with
-// the increment-form background update; the price is ~7 more FP instructions per point.
+// the plain sum 2 a0 u + sum a_k (...) loses that factor of fp32 precision to cancellation, while differences of
+// neighbouring values are exact (Sterbenz) and the rounding is then relative to the small differences.
+// fp32 numpy on cfg 2 (nt 4000, sharp model, increment-form background): receiver-data error vs the fp64 oracle
+// 1.6e-4 (plain) -> 6e-7 (all four terms as differences) -> 1.0e-6 (this form: k = 1, 2 only, ~4.5 fewer FP
+// instructions per point than the full difference form).
 template <int W>
 __device__ __forceinline__ void lap_points_w(const float* __restrict__ t, int tx, int ty, float2 (&L)[RZ][2],
                                              float2 (&C)[RZ][2]) {
@@ -179,6 +181,11 @@ __device__ __forceinline__ void lap_points_w(const float* __restrict__ t, int tx
     const float4 b = zw[r + R];
     const float4 c = ld4(row + 8);
     const float xs[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+    // first differences e_k = x[k+4] - x[k+3] (k = 0..4) shared by neighbouring points: the d = 1 term of point p
+    // is (x[p+1] - x[p]) + (x[p-1] - x[p]) = e_p - e_{p-1} (negation is exact: the same bits, 3 fewer FADDs a row)
+    float e[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) e[k] = __fsub_rn(xs[k + 4], xs[k + 3]);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int i = 2 * h;
@@ -189,15 +196,22 @@ __device__ __forceinline__ void lap_points_w(const float* __restrict__ t, int tx
       // differences are scalar FADDs (same roundings) written straight into the result pair
       auto DX = [&](int d) {
         if (d % 2 == 0) return add2(sub2(P(4 + d), ctr), sub2(P(4 - d), ctr));
+        if (d == 1) return make_float2(__fsub_rn(e[i + 1], e[i]), __fsub_rn(e[i + 2], e[i + 1]));
         return make_float2(__fadd_rn(__fsub_rn(xs[4 + d + i], xs[4 + i]), __fsub_rn(xs[4 - d + i], xs[4 + i])),
                            __fadd_rn(__fsub_rn(xs[5 + d + i], xs[5 + i]), __fsub_rn(xs[5 - d + i], xs[5 + i])));
       };
       auto DZ = [&](int d) { return add2(sub2(Z(4 + d), ctr), sub2(Z(4 - d), ctr)); };
+      // plain pair sums for the small outer weights (|a3|, |a4| <= 0.025): their rounding is 60x below the
+      // first two terms', which is where the cancellation happened
+      auto X = [&](int d) {
+        if (d % 2 == 0) return add2(P(4 - d), P(4 + d));
+        return make_float2(__fadd_rn(xs[4 - d + i], xs[4 + d + i]), __fadd_rn(xs[5 - d + i], xs[5 + d + i]));
+      };
       float2 s = mul2(splat2(HV_A1), add2(DX(1), DZ(1)));
       s = fma2(splat2(HV_A2), add2(DX(2), DZ(2)), s);
-      s = fma2(splat2(HV_A3), add2(DX(3), DZ(3)), s);
-      s = fma2(splat2(HV_A4), add2(DX(4), DZ(4)), s);
-      L[r][h] = s;
+      s = fma2(splat2(HV_A3), add2(X(3), add2(Z(1), Z(7))), s);
+      s = fma2(splat2(HV_A4), add2(X(4), add2(Z(0), Z(8))), s);
+      L[r][h] = fma2(splat2(-4.0f * (HV_A3 + HV_A4)), ctr, s);
       C[r][h] = ctr;
     }
   }

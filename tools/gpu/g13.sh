@@ -1,0 +1,10 @@
+# hybrid difference-form Laplacian: accuracy + speed
+set -x
+python tools/gpu/dbg_cfg2b.py > gpurun_out/g13_dbg.log 2>&1; cat gpurun_out/g13_dbg.log
+python tools/gpu/dbg_cfg2.py > gpurun_out/g13_dbg2.log 2>&1; cat gpurun_out/g13_dbg2.log
+timeout 900 python -m pytest tests/test_gpu_golden.py tests/test_gpu_parity.py -q -x > gpurun_out/g13_t.log 2>&1; echo t=$?
+tail -3 gpurun_out/g13_t.log
+timeout 300 python bench.py --config 3 --shots 16 --nt 400 --steps 3 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/g13_c3.json 2> gpurun_out/g13_c3.err; echo c3=$?
+python -c "import json;d=json.loads(open('gpurun_out/g13_c3.json').read().strip().splitlines()[-1]);print('c3', round(d['value'],3), {k:(round(v['avg_launch_ms']*1e3,1),round(v['batched_frac'],3)) for k,v in d['roofline']['kernels'].items()})"
+timeout 300 python bench.py --config 1 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/g13_c1.json 2> gpurun_out/g13_c1.err; echo c1=$?
+python -c "import json;d=json.loads(open('gpurun_out/g13_c1.json').read().strip().splitlines()[-1]);print('c1', round(d['value'],3), {k:(round(v['avg_launch_ms']*1e3,1),round(v['batched_frac'],3)) for k,v in d['roofline']['kernels'].items()})"

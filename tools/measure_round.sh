@@ -19,8 +19,8 @@ for S in 32 16 8; do
   timeout 600 python bench.py --config 3 --shots $S $E --no-e2e > gpurun_out/ev_cfg3_shots${S}_$TAG.json 2>&1; echo ev_shots$S=$?
 done
 # ncu launch list of the bench command (a window of launches after the warm-up steps)
-CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -s 100000 -c 8000 --csv \
+CMD="python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e"
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -s 2000 -c 6000 --csv \
     --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1; echo ncu_launch=$?
 P="python tools/profile_step.py --config 3 --shots 16 --nt 40 --reps 1"
 $P > gpurun_out/plain_prof_$TAG.log 2>&1 && \

@@ -72,7 +72,7 @@ if os.path.exists(lpath):
     tot = sum(sum(v) for v in per.values())
     with open(os.path.join(P, f"{a.tag}_launches.csv"), "w") as f:
         f.write(f"# ncu launch list (gpu__time_duration.sum, --clock-control none, cold-cache serialised), {a.tag}\n"
-                "# command: python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e ; ncu -s 100000 -c 8000\n"
+                "# command: python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e ; ncu -s 2000 -c 6000\n"
                 "kernel,launches,mean_us,share_of_listed_time\n")
         for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
             f.write(f"{k},{len(v)},{sum(v) / len(v):.2f},{sum(v) / tot:.4f}\n")

@@ -13,6 +13,8 @@ These are the fp64 oracle's answers for the exact launch plans the bench times, 
   cfg2_s31_grad.npy        gradient F*(F(m) - d_obs) of shot 31 at m (Eq. equ:grad)
   cfg2_s31_hv_k0.npy       H·v row of probe k = 0 for shot 31
   cfg2_s31_d_m.npz         d = F(m) of shot 31 at the evaluation model m (cfg 2 and cfg 3 share m and geometry)
+  cfg4_s127_nt1000_hv_k0.npy  cfg 4 grid (2048 x 6144), shot 127, probe 0, nt truncated to 1000 (SURVEY.md §8(d)
+                           parity sub-slice; the GPU runs it in CHECKPOINT mode with k = 32)
   meta.json                provenance: recipe, oracle calls, phi, timings, sha256 of oracle/wave.py
 
 Every value is computed in float64 by oracle.wave.Problem and rounded once to
@@ -86,10 +88,19 @@ def _cfg2_dm(_):
     return ("cfg2dm", CFG2_SHOT, d, time.time() - t0)
 
 
+def _cfg4(_):
+    import workloads as W
+    from oracle import wave
+    wl = W.config(4).subset(shots=[127], nt=1000)
+    t0 = time.time()
+    hv = wave.Problem(wl).hessvec_shot(0, [wl.probes([0])[0].astype(np.float64)], mode="checkpoint", ckpt=32)
+    return ("cfg4", 127, hv[0], time.time() - t0)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workers", type=int, default=6)
-    ap.add_argument("--only", default="cfg1,cfg2,cfg3,cfg2dm")
+    ap.add_argument("--only", default="cfg1,cfg2,cfg3,cfg2dm,cfg4")
     a = ap.parse_args()
     only = set(a.only.split(","))
     os.makedirs(OUT, exist_ok=True)
@@ -102,6 +113,8 @@ def main():
         tasks += [(_cfg1_shot, s) for s in range(16)]
     if "cfg2dm" in only:
         tasks += [(_cfg2_dm, 0)]
+    if "cfg4" in only:
+        tasks += [(_cfg4, 0)]
     t0 = time.time()
     res = {}
     with Pool(a.workers) as pool:
@@ -149,6 +162,12 @@ def main():
         np.savez_compressed(os.path.join(OUT, "cfg2_s31_d_m.npz"), d=d.astype(np.float32))
         meta["cfg2_s31_d_m"] = {**common, "config": 2, "shot": CFG2_SHOT,
                                 "call": "Problem(config(2)).forward(31) (the evaluation model m)", "cpu_s": secs}
+    if "cfg4" in only:
+        hv0, secs = res[("cfg4", 127)]
+        np.save(os.path.join(OUT, "cfg4_s127_nt1000_hv_k0.npy"), hv0.astype(np.float32))
+        meta["cfg4_s127_nt1000"] = {**common, "config": 4, "shot": 127, "probes": [0], "nt": 1000,
+                                    "call": "Problem(config(4).subset(shots=[127], nt=1000)).hessvec_shot(0, [probe 0], "
+                                            "mode='checkpoint', ckpt=32)", "cpu_s": secs}
     with open(mpath, "w") as f:
         json.dump(meta, f, indent=1, sort_keys=True)
     print("done", time.time() - t0)

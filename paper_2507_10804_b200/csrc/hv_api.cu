@@ -50,7 +50,10 @@ int make_tmap(hv_ctx* c, const float* base, long long nplanes, int box_w, int bo
 constexpr bool kTwoStepDefault = false;  // T = 2 forward (fwd_t2_kernel) by default
 constexpr bool kT2BwdDefault = true;     // with it, the T = 2 adjoint (bwd_t2_kernel) for FULL-store calls
 constexpr int kPhiBlocks = 1024;  // residual kernel grid: fixed, so phi's summation order never changes
-constexpr int kQresFG = 6;  // resident-q forward: Born fields per CTA (6 q_k tiles + 3 stages: 2 CTAs per SM)
+#ifndef HV_QRES_FG
+#define HV_QRES_FG 6
+#endif
+constexpr int kQresFG = HV_QRES_FG;  // resident-q forward: Born fields per CTA (6 q_k tiles + 3 stages: 2 CTAs/SM)
 // Backward CTAs per (tile, field group): the batch's shots are split into this many parts, each summing its
 // imaging terms into its own accumulator copy (finalize adds the copies in a fixed order). 2 halves the last
 // partial wave of the backward grid at the cost of one more RED per point and field per launch; measured on
@@ -462,7 +465,7 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     fp.qfg = std::min(K > 0 ? K : 1, kQresFG);
     if (const char* qf = std::getenv("HV_QFG")) fp.qfg = std::max(1, std::min({K > 0 ? K : 1, 16, std::atoi(qf)}));
     const int Gq = K > 0 ? (K + fp.qfg - 1) / fp.qfg : 1;
-    const int qres_smem = STAGES_BYTES + BAR_BYTES + fp.qfg * PT_BYTES;
+    const int qres_smem = QSTAGES_BYTES + BAR_BYTES + fp.qfg * PT_BYTES;
     if (phase == 0 && use_t2) {
       T2Params t2{};
       t2.g = g;
@@ -964,7 +967,7 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
       cudaFuncSetAttribute(bwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_BYTES) !=
           cudaSuccess ||
       cudaFuncSetAttribute(fwd_qres_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           STAGES_BYTES + BAR_BYTES + 16 * PT_BYTES) != cudaSuccess ||
+                           QSTAGES_BYTES + BAR_BYTES + 16 * PT_BYTES) != cudaSuccess ||
       cudaFuncSetAttribute(fwd_t2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t2_fwd_smem_bytes()) !=
           cudaSuccess ||
       cudaFuncSetAttribute(bwd_t2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t2_bwd_smem_bytes()) !=

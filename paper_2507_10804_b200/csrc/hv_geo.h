@@ -30,6 +30,13 @@ constexpr int NSTAGE = HV_NSTAGE;             // TMA pipeline depth (items in fl
 // one pipeline stage: halo of level n (stencil input) + pointwise tile of level n-1 (updated in place)
 constexpr int STAGE_FLOATS = TILE_FLOATS + PT_FLOATS;
 constexpr int STAGES_BYTES = NSTAGE * STAGE_FLOATS * 4;
+// resident-q forward: its own stage count (fewer stages leave room for more resident q_k tiles, i.e. fewer
+// background recomputes per shot)
+#ifndef HV_NSTAGE_Q
+#define HV_NSTAGE_Q 3
+#endif
+constexpr int NSTAGE_Q = HV_NSTAGE_Q;
+constexpr int QSTAGES_BYTES = NSTAGE_Q * STAGE_FLOATS * 4;
 constexpr int BAR_BYTES = 128;              // keeps the q tiles behind the barriers 128-byte aligned (TMA)
 // forward CTA: NSTAGE_F stages of halo u^n + tile u^{n-1} + tile q_k
 #ifndef HV_NSTAGE_F

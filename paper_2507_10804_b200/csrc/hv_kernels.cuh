@@ -609,6 +609,15 @@ __device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages
 #ifndef HV_FWD_MINB
 #define HV_FWD_MINB MINB
 #endif
+#ifndef HV_BWD_SJ_LAST
+#define HV_BWD_SJ_LAST 1  // measured: backward 584 -> 566 us per cfg 3 launch, DRAM reads -150 MB
+#endif
+#ifndef HV_BWD_PREV_FIRST
+#define HV_BWD_PREV_FIRST 0
+#endif
+#ifndef HV_QRES_HINTS
+#define HV_QRES_HINTS 0
+#endif
 #ifndef HV_BWD_MINB
 #define HV_BWD_MINB MINB
 #endif
@@ -668,22 +677,35 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
   const int nitems = p.S * (1 + nf);                  // per shot: background, then its Born fields
   const int par_n = p.n & 1, par_new = par_n ^ 1;
   const bool leader = (grp == 0) && p.bg_update;
-  uint64_t* qbar = bars + NSTAGE;
+  uint64_t* qbar = bars + NSTAGE_Q;
 
   // producer (thread 0): next item (ps, pt) -> stage
   int ps = 0, pt = 0, issued = 0;
-  Ring prod;
+  RingN<NSTAGE_Q> prod;
   auto issue_next = [&]() {
     float* st = stages + prod.stage * STAGE_FLOATS;
     const bool upd = pt > 0 || leader;
     const int slot = pt == 0 ? p.bg_slot : p.born_slot0 + fb + pt - 1;
     const int pl = (ps * p.nslot + slot) * 2;
     mbar_expect_tx(&bars[prod.stage], TILE_BYTES + (upd ? PT_BYTES : 0));
+#if HV_QRES_HINTS
+    // the background halo of a shot is read by every field group's CTA of the tile (different waves): evict_last;
+    // the level n-1 / D tiles are single-use: evict_first
+    if (pt == 0)
+      tma_load_3d_hint(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_n, policy_evict_last());
+    else
+      tma_load_3d(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_n);
+    if (upd && pt == 0)  // background: D^n (increment form)
+      tma_load_3d_hint(st + TILE_FLOATS, md, &bars[prod.stage], x0, z0, (p.dplane0 + ps) * 2, policy_evict_first());
+    else if (upd)
+      tma_load_3d_hint(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_new, policy_evict_first());
+#else
     tma_load_3d(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_n);
     if (upd && pt == 0)  // background: D^n (increment form)
       tma_load_3d(st + TILE_FLOATS, md, &bars[prod.stage], x0, z0, (p.dplane0 + ps) * 2);
     else if (upd)
       tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_new);
+#endif
     prod.advance();
     if (++pt > nf) {
       pt = 0;
@@ -696,7 +718,7 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
       mbar_expect_tx(qbar, nf * PT_BYTES);
       for (int t = 0; t < nf; ++t) tma_load_3d(qs + t * PT_FLOATS, mq, qbar, x0, z0, fb + t);
     }
-    while (issued < min(NSTAGE, nitems)) issue_next();
+    while (issued < min(NSTAGE_Q, nitems)) issue_next();
   }
 
   const int I0 = z0 + ty * RZ;
@@ -720,8 +742,8 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
   const long long data_stride = static_cast<long long>(g.nt) * g.nrec;
   if (nf > 0) mbar_wait(qbar, 0);
 
-  Ring cons;
-  // a block barrier per item, then thread 0 refills the stage just consumed (NSTAGE items of lead). Per-warp
+  RingN<NSTAGE_Q> cons;
+  // a block barrier per item, then thread 0 refills the stage just consumed (NSTAGE_Q items of lead). Per-warp
   // release (empty mbarriers, refill of item c - 1 after item c) measured slower here: 698 vs 594 us per launch
   // on cfg 3 (the refill lost one item of lead and thread 0 waited on the slowest warp).
   auto release = [&]() {
@@ -854,13 +876,13 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
                     const FwdParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stages = reinterpret_cast<float*>(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + STAGES_BYTES);
-  float* qs = reinterpret_cast<float*>(smem_raw + STAGES_BYTES + BAR_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + QSTAGES_BYTES);
+  float* qs = reinterpret_cast<float*>(smem_raw + QSTAGES_BYTES + BAR_BYTES);
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     tma_prefetch_desc(&mh);
     tma_prefetch_desc(&mt);
     tma_prefetch_desc(&mq);
-    for (int i = 0; i < NSTAGE + 1; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < NSTAGE_Q + 1; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -925,10 +947,22 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
     const bool with_sj = p.imaging && pt == 0;  // s^j of the shot travels with its first field's stage
     mbar_expect_tx(&bars[prod.stage], TILE_BYTES + (p.update ? PT_BYTES : 0) + (with_sj ? PT_BYTES : 0));
     tma_load_3d(st, mh, &bars[prod.stage], x0 - R, z0 - R, pl + par_in);
+#if HV_BWD_PREV_FIRST
+    if (p.update)  // lambda^{j+2}: single use
+      tma_load_3d_hint(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_prev, policy_evict_first());
+#else
     if (p.update) tma_load_3d(st + TILE_FLOATS, mt, &bars[prod.stage], x0, z0, pl + par_prev);
-    if (with_sj)  // interior store: padded (x0, z0) is interior (x0 - c0, z0 - W); outside -> TMA zero fill
-      tma_load_3d(st + TILE_FLOATS + PT_FLOATS, msj, &bars[prod.stage], x0 - g.c0, z0 - g.W,
-                  static_cast<int>(p.sj_plane0 + static_cast<long long>(ps) * p.sj_shot_planes));
+#endif
+    if (with_sj) {  // interior store: padded (x0, z0) is interior (x0 - c0, z0 - W); outside -> TMA zero fill
+      const int sj_plane = static_cast<int>(p.sj_plane0 + static_cast<long long>(ps) * p.sj_shot_planes);
+#if HV_BWD_SJ_LAST
+      // s^j of a shot is read by every field group's CTA of the tile, in different waves: keep it in L2
+      tma_load_3d_hint(st + TILE_FLOATS + PT_FLOATS, msj, &bars[prod.stage], x0 - g.c0, z0 - g.W, sj_plane,
+                       policy_evict_last());
+#else
+      tma_load_3d(st + TILE_FLOATS + PT_FLOATS, msj, &bars[prod.stage], x0 - g.c0, z0 - g.W, sj_plane);
+#endif
+    }
     prod.advance();
     if (++pt == nf) {
       pt = 0;

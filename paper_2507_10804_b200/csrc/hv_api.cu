@@ -53,7 +53,8 @@ constexpr int kPhiBlocks = 1024;  // residual kernel grid: fixed, so phi's summa
 #ifndef HV_QRES_FG
 #define HV_QRES_FG 6
 #endif
-constexpr int kQresFG = HV_QRES_FG;  // resident-q forward: Born fields per CTA (6 q_k tiles + 3 stages: 2 CTAs/SM)
+constexpr int kQresFG = HV_QRES_FG;
+constexpr int kQresOrder = 0;  // fwd_qres_kernel grid order (FwdParams::qorder)  // resident-q forward: Born fields per CTA (6 q_k tiles + 3 stages: 2 CTAs/SM)
 // Backward CTAs per (tile, field group): the batch's shots are split into this many parts, each summing its
 // imaging terms into its own accumulator copy (finalize adds the copies in a fixed order). 2 halves the last
 // partial wave of the backward grid at the cost of one more RED per point and field per launch; measured on
@@ -452,6 +453,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     fp.ring_shot_stride = ringN * g.nt;
     fp.dbuf = bgD;
     fp.dplane0 = 0;
+    fp.qorder = kQresOrder;
+    if (const char* qo = std::getenv("HV_QRES_ORDER")) fp.qorder = std::atoi(qo);  // tuning
     if (boundary && phase == 0) CU_TRY(cudaMemsetAsync(ring, 0, sizeof(float) * ringN * g.nt * Sb, c->stream));
     fp.G = Gf;
     // unit order: one shot per block while Q stays L2-resident; otherwise as many shots per block as keep the
@@ -521,8 +524,8 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
         fp.s_out = full ? store + (size_t)n * g.iplane : nullptr;
         fp.ring_out = boundary ? ring + (size_t)(n + 1) * ringN : nullptr;
         if (qres)
-          fwd_qres_kernel<<<dim3(g.ntx, g.ntz, Gq), block, qres_smem, c->stream>>>(map_halo, map_tile, map_q, map_d,
-                                                                                    fp);
+          fwd_qres_kernel<<<dim3(g.ntx * g.ntz * Gq), block, qres_smem, c->stream>>>(map_halo, map_tile, map_q,
+                                                                                      map_d, fp);
         else
           fwd_step_kernel<<<gridf, block, fwd_smem, c->stream>>>(map_halo, map_tile, map_q, map_w, map_d, fp);
         launches++;

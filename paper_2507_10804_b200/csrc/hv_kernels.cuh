@@ -284,6 +284,8 @@ struct FwdParams {
   // of the D tensor map / buffer dbuf ([.][2][Nz][P]; the second plane of a pair is used by the T = 2 kernel).
   float* dbuf;
   int dplane0;
+  int qorder;             // fwd_qres_kernel linear grid order: 0 = tiles (x, then z) fastest, group slowest;
+                          // 1 = group fastest (the groups of a tile share its background halo in L2)
 };
 
 // Per-point damping of this thread's points (SP: the tile touches the sponge): (1 - c) and 1 / (1 + c), as
@@ -667,11 +669,10 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
 template <bool SP>
 __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUtensorMap* mt, const CUtensorMap* mq,
                                          const CUtensorMap* md, const FwdParams& p, float* stages, float* qs,
-                                         uint64_t* bars) {
+                                         uint64_t* bars, int bx, int by, int grp) {
   const Geo& g = p.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
-  const int x0 = blockIdx.x * TX, z0 = blockIdx.y * TZ;
-  const int grp = blockIdx.z;
+  const int x0 = bx * TX, z0 = by * TZ;
   const int fb = grp * p.qfg;
   const int nf = max(0, min(p.K, fb + p.qfg) - fb);   // Born fields of this CTA
   const int nitems = p.S * (1 + nf);                  // per shot: background, then its Born fields
@@ -736,7 +737,7 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
   for (int r = 0; r < RZ; ++r) row_ok[r] = !SP || I0 + r < g.Nz;
   Damp<SP> dmp;
   dmp.init(g, I0, J0);
-  const int tile_id = blockIdx.y * g.ntx + blockIdx.x;
+  const int tile_id = by * g.ntx + bx;
   const int rb = p.trec_beg[tile_id], re = p.trec_beg[tile_id + 1];
   const float amp = p.src_amp[p.n];
   const long long data_stride = static_cast<long long>(g.nt) * g.nrec;
@@ -886,10 +887,20 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
     fence_mbar_init();
   }
   __syncthreads();
-  if (tile_is_interior(p.g, blockIdx.x * TX, blockIdx.y * TZ))
-    fwd_qres_body<false>(&mh, &mt, &mq, &md, p, stages, qs, bars);
+  // linear grid of ntx * ntz * G CTAs
+  const int ntl = p.g.ntx * p.g.ntz;
+  const int G = (gridDim.x + ntl - 1) / ntl;
+  int grp, tile;
+  if (p.qorder == 1) {
+    grp = blockIdx.x % G, tile = blockIdx.x / G;
+  } else {
+    grp = blockIdx.x / ntl, tile = blockIdx.x - grp * ntl;
+  }
+  const int by = tile / p.g.ntx, bx = tile - by * p.g.ntx;
+  if (tile_is_interior(p.g, bx * TX, by * TZ))
+    fwd_qres_body<false>(&mh, &mt, &mq, &md, p, stages, qs, bars, bx, by, grp);
   else
-    fwd_qres_body<true>(&mh, &mt, &mq, &md, p, stages, qs, bars);
+    fwd_qres_body<true>(&mh, &mt, &mq, &md, p, stages, qs, bars, bx, by, grp);
 }
 
 // ------------------------------------------------------------------------------------------------ backward

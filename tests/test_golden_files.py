@@ -32,6 +32,8 @@ def test_shapes(meta):
     for f in ("cfg3_hv_k0_k16_s16-32.npy", "cfg3_hv_k0_k16_s31.npy"):
         assert np.load(os.path.join(GOLD, f)).shape == (2, 384, 1152)
     assert np.load(os.path.join(GOLD, "cfg2_s31_dobs.npz"))["d_obs"].shape == (4000, 1152)
+    assert np.load(os.path.join(GOLD, "cfg2_s31_d_m.npz"))["d"].shape == (4000, 1152)
+    assert np.load(os.path.join(GOLD, "cfg4_s127_nt1000_hv_k0.npz"))["hv"].shape == (2048, 6144)
     assert meta["cfg1_hv_k27_k50"]["shots"] == list(range(16))
     assert meta["cfg3_hv_k0_k16"]["shots"] == list(range(16, 32))
 
@@ -67,4 +69,12 @@ def test_cfg2_gradient_and_hv(meta):
     hv0 = np.load(os.path.join(GOLD, "cfg2_s31_hv_k0.npy")).astype(np.float64)
     g = np.load(os.path.join(GOLD, "cfg2_s31_grad.npy"))
     assert meta["cfg2_s31"]["phi"] > 0 and np.isfinite(g).all() and np.abs(g).max() > 0
+    assert float(np.sum(v0 * hv0)) > 0
+
+
+def test_cfg4_row_psd():
+    """<v_0, H v_0> > 0 for the cfg 4 grid slice (shot 127, nt 1000)."""
+    wl = W.config(4)
+    v0 = wl.probes([0])[0].astype(np.float64)
+    hv0 = np.load(os.path.join(GOLD, "cfg4_s127_nt1000_hv_k0.npz"))["hv"].astype(np.float64)
     assert float(np.sum(v0 * hv0)) > 0

@@ -117,7 +117,7 @@ def test_cfg4_grid_checkpoint_nt1000(hv):
     """cfg 4 grid (2048 x 6144, 12.9 M padded points), shot 127, probe 0, nt truncated to 1000, CHECKPOINT mode
     with k = 32 (SURVEY.md §8(d) parity sub-slice: the storage mode BJ cfg 4 mandates)."""
     wl = W.config(4).subset(shots=[127], nt=1000)
-    gold = _gold("cfg4_s127_nt1000_hv_k0.npy")
+    gold = _gold("cfg4_s127_nt1000_hv_k0.npz").astype(np.float64)
     s = hv.Solver.from_workload(wl, store="checkpoint", ckpt_interval=32)
     out = s.hessvec(wl.model, wl.probes([0]))
     st = s.stats()

@@ -13,7 +13,7 @@ These are the fp64 oracle's answers for the exact launch plans the bench times, 
   cfg2_s31_grad.npy        gradient F*(F(m) - d_obs) of shot 31 at m (Eq. equ:grad)
   cfg2_s31_hv_k0.npy       H·v row of probe k = 0 for shot 31
   cfg2_s31_d_m.npz         d = F(m) of shot 31 at the evaluation model m (cfg 2 and cfg 3 share m and geometry)
-  cfg4_s127_nt1000_hv_k0.npy  cfg 4 grid (2048 x 6144), shot 127, probe 0, nt truncated to 1000 (SURVEY.md §8(d)
+  cfg4_s127_nt1000_hv_k0.npz  cfg 4 grid (2048 x 6144), shot 127, probe 0, nt truncated to 1000 (SURVEY.md §8(d)
                            parity sub-slice; the GPU runs it in CHECKPOINT mode with k = 32)
   meta.json                provenance: recipe, oracle calls, phi, timings, sha256 of oracle/wave.py
 
@@ -164,7 +164,7 @@ def main():
                                 "call": "Problem(config(2)).forward(31) (the evaluation model m)", "cpu_s": secs}
     if "cfg4" in only:
         hv0, secs = res[("cfg4", 127)]
-        np.save(os.path.join(OUT, "cfg4_s127_nt1000_hv_k0.npy"), hv0.astype(np.float32))
+        np.savez_compressed(os.path.join(OUT, "cfg4_s127_nt1000_hv_k0.npz"), hv=hv0.astype(np.float32))
         meta["cfg4_s127_nt1000"] = {**common, "config": 4, "shot": 127, "probes": [0], "nt": 1000,
                                     "call": "Problem(config(4).subset(shots=[127], nt=1000)).hessvec_shot(0, [probe 0], "
                                             "mode='checkpoint', ckpt=32)", "cpu_s": secs}

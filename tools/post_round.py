@@ -35,14 +35,21 @@ try:
         traffic = {"records": []}
 except Exception:
     traffic = {"records": []}
-for short in ("fwd", "bwd"):
-    rep = os.path.join(G, f"prof_{short}_{a.tag}.ncu-rep")
+CAPTURES = [  # (report stem, summary name, workload, shot batch, K, command)
+    ("fwd", "fwd", a.workload, a.shot_batch, a.K, "tools/profile_step.py --config 3 --shots 16 --nt 40"),
+    ("bwd", "bwd", a.workload, a.shot_batch, a.K, "tools/profile_step.py --config 3 --shots 16 --nt 40"),
+    ("fwd_cfg4", "cfg4grid_fwd", "cfg4", 4, 64,
+     "tools/profile_step.py --config 4 --shots 4 --nt 12"),
+    ("bwd_cfg4", "cfg4grid_bwd", "cfg4", 4, 64,
+     "tools/profile_step.py --config 4 --shots 4 --nt 12"),
+]
+for stem, short, workload, sb, K, cmd in CAPTURES:
+    rep = os.path.join(G, f"prof_{stem}_{a.tag}.ncu-rep")
     if not os.path.exists(rep):
         continue
     res = summarise(rep)
     with open(os.path.join(P, f"{a.tag}_ncu_{short}.txt"), "w") as f:
-        f.write(f"# ncu --set full --clock-control none, {a.workload} S={a.shot_batch} K={a.K} "
-                f"(tools/profile_step.py --config 3 --shots 16 --nt 40), {a.tag}\n")
+        f.write(f"# ncu --set full --clock-control none, {workload} S={sb} K={K} ({cmd}), {a.tag}\n")
         for d in res:
             f.write(f"--- {d['kernel']}\n")
             for k in KEYS:
@@ -52,8 +59,8 @@ for short in ("fwd", "bwd"):
         b = (d["dram__bytes_read.sum"] * UNIT[d["dram__bytes_read.sum@unit"]] +
              d["dram__bytes_write.sum"] * UNIT[d["dram__bytes_write.sum@unit"]])
         t = d["gpu__time_duration.sum"] * (1e-3 if d["gpu__time_duration.sum@unit"] == "ns" else 1.0)
-        rec = {"kernel": d["kernel"].replace("hvk::", ""), "workload": a.workload, "shot_batch": a.shot_batch,
-               "K": a.K, "dram_bytes_per_launch": b, "duration_us_ncu": t,
+        rec = {"kernel": d["kernel"].replace("hvk::", ""), "workload": workload, "shot_batch": sb,
+               "K": K, "dram_bytes_per_launch": b, "duration_us_ncu": t,
                "source": f"ncu --set full, {a.tag} (profiles/{a.tag}_ncu_{short}.txt)"}
         traffic["records"] = [r for r in traffic["records"]
                               if not (r["kernel"] == rec["kernel"] and r["workload"] == rec["workload"]

@@ -58,7 +58,7 @@ for stem, short, workload, sb, K, cmd in CAPTURES:
     for d in res:
         b = (d["dram__bytes_read.sum"] * UNIT[d["dram__bytes_read.sum@unit"]] +
              d["dram__bytes_write.sum"] * UNIT[d["dram__bytes_write.sum@unit"]])
-        t = d["gpu__time_duration.sum"] * (1e-3 if d["gpu__time_duration.sum@unit"] == "ns" else 1.0)
+        t = d["gpu__time_duration.sum"] * {"ns": 1e-3, "us": 1.0, "ms": 1e3}.get(d["gpu__time_duration.sum@unit"], 1.0)
         rec = {"kernel": d["kernel"].replace("hvk::", ""), "workload": workload, "shot_batch": sb,
                "K": K, "dram_bytes_per_launch": b, "duration_us_ncu": t,
                "source": f"ncu --set full, {a.tag} (profiles/{a.tag}_ncu_{short}.txt)"}

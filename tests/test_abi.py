@@ -63,3 +63,18 @@ def test_product_never_imports_the_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", src, flags=re.M), f
                 assert "oracle/" not in src.replace("`oracle/`", ""), f
+
+
+def test_nccl_helpers_without_gpu():
+    """The in-library NCCL path dlopens libnccl.so.2: a unique id is available on the CPU host; creating a
+    communicator without a device fails loudly (HV_ECUDA) instead of hanging or falling back."""
+    import torch
+    uid = hv.nccl_unique_id()
+    assert len(uid) == 128 and any(uid)
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(hv.HVError) as e:
+        hv.nccl_comm_create(1, 0, uid, 0)
+    assert e.value.status == hv.HV_ECUDA
+    with pytest.raises(ValueError):
+        hv.nccl_comm_create(1, 0, b"short", 0)

@@ -86,6 +86,13 @@ def test_in_library_nccl_one_rank(hv, case):
         d_obs = np.zeros((case.ns, case.nt, case.nrec), np.float32)
         s2 = hv.Solver.from_workload(case)
         assert s.gradient(case.model, d_obs)[0] == s2.gradient(case.model, d_obs)[0]
+        phi_c = s.misfit(case.model, d_obs)
+        assert phi_c == s2.misfit(case.model, d_obs)
+        # the eigensolver's batched H·v go through the same in-library reduction
+        Om = np.random.default_rng(3).standard_normal((6, case.nz, case.nx)).astype(np.float32)
+        ev_c, _ = s.lowrank_geneig(case.model, Om, 3, power_iters=1)
+        ev_r, _ = s2.lowrank_geneig(case.model, Om, 3, power_iters=1)
+        assert np.array_equal(ev_c, ev_r)
         s.set_comm(None)
         assert np.array_equal(s.hessvec(case.model, V), ref)
         s.close()

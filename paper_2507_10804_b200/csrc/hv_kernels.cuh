@@ -167,7 +167,12 @@ __device__ __forceinline__ float2 half2of(const float4& v, int h) { return h == 
 // fp32 numpy on cfg 2 (nt 4000, sharp model, increment-form background): receiver-data error vs the fp64 oracle
 // 1.6e-4 (plain) -> 6e-7 (all four terms as differences) -> 1.0e-6 (this form: k = 1, 2 only, ~4.5 fewer FP
 // instructions per point than the full difference form).
-template <int W>
+// DIFF = false: the plain form 2 a0 u + sum_k a_k (pair sums), ~5 fewer FP instructions per point, kept for
+// experiments only. Measured on cfg 2 shot 31 at nt 4000 (H·v row 0 / gradient vs the fp64 oracle): DIFF for every
+// field 2.4e-5 / 5.2e-6 (the default); plain for Born and adjoint fields 1.1e-5 / 2.3e-4 (the gradient's adjoint,
+// driven by the residual at every step, needs DIFF); plain for the Born fields only 6.0e-5 / 5.2e-6 — and only
+// 1 % faster at cfg 3, so every field uses DIFF.
+template <int W, bool DIFF = true>
 __device__ __forceinline__ void lap_points_w(const float* __restrict__ t, int tx, int ty, float2 (&L)[RZ][2],
                                              float2 (&C)[RZ][2]) {
   const int col = R + tx * 4;
@@ -181,6 +186,26 @@ __device__ __forceinline__ void lap_points_w(const float* __restrict__ t, int tx
     const float4 b = zw[r + R];
     const float4 c = ld4(row + 8);
     const float xs[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+    if constexpr (!DIFF) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = 2 * h;
+        auto P = [&](int k) { return make_float2(xs[k + i], xs[k + i + 1]); };
+        auto Z = [&](int k) { return half2of(zw[r + k], h); };
+        auto X = [&](int d) {
+          if (d % 2 == 0) return add2(P(4 - d), P(4 + d));
+          return make_float2(__fadd_rn(xs[4 - d + i], xs[4 + d + i]), __fadd_rn(xs[5 - d + i], xs[5 + d + i]));
+        };
+        const float2 ctr = P(4);
+        float2 s = mul2(splat2(HV_A1), add2(X(1), add2(Z(3), Z(5))));
+        s = fma2(splat2(HV_A2), add2(X(2), add2(Z(2), Z(6))), s);
+        s = fma2(splat2(HV_A3), add2(X(3), add2(Z(1), Z(7))), s);
+        s = fma2(splat2(HV_A4), add2(X(4), add2(Z(0), Z(8))), s);
+        L[r][h] = fma2(splat2(2.0f * HV_A0), ctr, s);
+        C[r][h] = ctr;
+      }
+      continue;
+    }
     // first differences e_k = x[k+4] - x[k+3] (k = 0..4) shared by neighbouring points: the d = 1 term of point p
     // is (x[p+1] - x[p]) + (x[p-1] - x[p]) = e_p - e_{p-1} (negation is exact: the same bits, 3 fewer FADDs a row)
     float e[5];
@@ -217,8 +242,16 @@ __device__ __forceinline__ void lap_points_w(const float* __restrict__ t, int tx
   }
 }
 __device__ __forceinline__ void lap_points(const float* __restrict__ t, int tx, int ty, float2 (&L)[RZ][2],
-                                           float2 (&C)[RZ][2]) {
-  lap_points_w<HX>(t, tx, ty, L, C);
+                                           float2 (&C)[RZ][2]) {  // Born fields (forward)
+  lap_points_w<HX, true>(t, tx, ty, L, C);
+}
+__device__ __forceinline__ void lap_points_adj(const float* __restrict__ t, int tx, int ty, float2 (&L)[RZ][2],
+                                               float2 (&C)[RZ][2]) {  // adjoint fields: the gradient's needs DIFF
+  lap_points_w<HX, true>(t, tx, ty, L, C);
+}
+__device__ __forceinline__ void lap_points_bg(const float* __restrict__ t, int tx, int ty, float2 (&L)[RZ][2],
+                                              float2 (&C)[RZ][2]) {  // background field
+  lap_points_w<HX, true>(t, tx, ty, L, C);
 }
 
 // Sponge coefficient c = kc (d_z^2 + d_x^2), d_z = max(0, W - I, I - (W + nz - 1)) (C10).
@@ -521,7 +554,7 @@ __device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages
       w[r][0] = lo2(wv), w[r][1] = hi2(wv);
     }
     float2 C[RZ][2];
-    lap_points(st, tx, ty, Lb, C);
+    lap_points_bg(st, tx, ty, Lb, C);
     if (leader) {
       float* dst = p.pool + (static_cast<long long>(s * p.nslot + p.bg_slot) * 2 + par_new) * g.plane;
       float* dD = p.dbuf + static_cast<long long>((p.dplane0 + s) * 2) * g.plane;
@@ -778,7 +811,7 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
       const float* st = stages + cons.stage * STAGE_FLOATS;
       mbar_wait(&bars[cons.stage], cons.phase);
       float2 C[RZ][2];
-      lap_points(st, tx, ty, Lb, C);
+      lap_points_bg(st, tx, ty, Lb, C);
       if (leader) {
         float* dst = p.pool + (static_cast<long long>(s * p.nslot + p.bg_slot) * 2 + par_new) * g.plane;
         float* dD = p.dbuf + static_cast<long long>((p.dplane0 + s) * 2) * g.plane;
@@ -1049,7 +1082,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
       }
 #if HV_BWD_PAIRED
       float2 L2[RZ][2], C2[RZ][2];
-      lap_points(st, tx, ty, L2, C2);
+      lap_points_adj(st, tx, ty, L2, C2);
       if (p.update) {
 #pragma unroll
         for (int r = 0; r < RZ; ++r) {
@@ -1077,7 +1110,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
       float L[RZ][4], C[RZ][4];
       {
         float2 L2[RZ][2], C2[RZ][2];
-        lap_points(st, tx, ty, L2, C2);
+        lap_points_adj(st, tx, ty, L2, C2);
 #pragma unroll
         for (int r = 0; r < RZ; ++r)
 #pragma unroll
@@ -1236,7 +1269,7 @@ __device__ __forceinline__ void rev_body(const CUtensorMap* mh, const CUtensorMa
     const float* st = stages + cons.stage * STAGE_FLOATS;
     mbar_wait(&bars[cons.stage], cons.phase);
     float2 L2[RZ][2], C2[RZ][2];
-    lap_points(st, tx, ty, L2, C2);
+    lap_points_bg(st, tx, ty, L2, C2);
     float L[RZ][4], C[RZ][4];
 #pragma unroll
     for (int r = 0; r < RZ; ++r)

@@ -214,7 +214,7 @@ __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtenso
       float* mid = midb + (it & 1) * T2_MID_FLOATS;
       mbar_wait(&bars[cons.stage], cons.phase);
       float2 C0[RZ][2];
-      lap_points_w<T2_IX>(st, tx, ty, Lb0, C0);
+      lap_points_w<T2_IX, true>(st, tx, ty, Lb0, C0);
       const int sI = p.src_I[p.shot0 + s], sJ = p.src_J[p.shot0 + s];
       float v1s[RZ][4], d1s[RZ][4];  // u^{n+1}, D^{n+1} at this thread's points
 #pragma unroll
@@ -241,7 +241,7 @@ __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtenso
       barrier_and_refill();
       if (inner) {
         float2 C1[RZ][2];
-        lap_points_w<T2_MX>(mid - R * T2_MX - R, tx, ty, Lb1, C1);
+        lap_points_w<T2_MX, true>(mid - R * T2_MX - R, tx, ty, Lb1, C1);
         if (leader) {
           float* d1 = p.pool + (static_cast<long long>(s * p.nslot) * 4 + l1) * g.plane;
           float* d2 = p.pool + (static_cast<long long>(s * p.nslot) * 4 + l2) * g.plane;
@@ -312,7 +312,7 @@ __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtenso
       const float* qk = qs + t * T2_MID_FLOATS + so;
       mbar_wait(&bars[cons.stage], cons.phase);
       float2 L0[RZ][2], C0[RZ][2];
-      lap_points_w<T2_IX>(st, tx, ty, L0, C0);
+      lap_points_w<T2_IX, true>(st, tx, ty, L0, C0);
       float v1s[RZ][4];
 #pragma unroll
       for (int r = 0; r < RZ; ++r) {
@@ -330,7 +330,7 @@ __device__ __forceinline__ void fwd_t2_body(const CUtensorMap* mh, const CUtenso
       barrier_and_refill();
       if (inner) {
         float2 L1[RZ][2], C1[RZ][2];
-        lap_points_w<T2_MX>(mid - R * T2_MX - R, tx, ty, L1, C1);
+        lap_points_w<T2_MX, true>(mid - R * T2_MX - R, tx, ty, L1, C1);
         const long long pl = static_cast<long long>(s * p.nslot + p.born_slot0 + fb + t) * 4;
         float* d1 = p.pool + (pl + l1) * g.plane;
         float* d2 = p.pool + (pl + l2) * g.plane;
@@ -577,7 +577,7 @@ __device__ __forceinline__ void bwd_t2_body(const CUtensorMap* mh, const CUtenso
         }
       }
       float2 L0[RZ][2], C0[RZ][2];
-      lap_points_w<T2_IX>(st, tx, ty, L0, C0);
+      lap_points_w<T2_IX, true>(st, tx, ty, L0, C0);
       float v1s[RZ][4];
 #pragma unroll
       for (int r = 0; r < RZ; ++r) {
@@ -618,7 +618,7 @@ __device__ __forceinline__ void bwd_t2_body(const CUtensorMap* mh, const CUtenso
         float* d0 = p.pool + (static_cast<long long>(s * p.nslot + p.slot0 + fb + f) * 4 + l0) * g.plane;
         if (two) {
           float2 L1[RZ][2], C1[RZ][2];
-          lap_points_w<T2_MX>(mid - R * T2_MX - R, tx, ty, L1, C1);
+          lap_points_w<T2_MX, true>(mid - R * T2_MX - R, tx, ty, L1, C1);
           float* d1 = p.pool + (static_cast<long long>(s * p.nslot + p.slot0 + fb + f) * 4 + l1) * g.plane;
 #pragma unroll
           for (int r = 0; r < RZ; ++r) {

@@ -463,7 +463,7 @@ def main():
         f_launch_ms = float(np.mean(fwd_ms)) / (nbatch * (wl.nt - 1))
         b_launch_ms = float(np.mean(bwd_ms)) / (nbatch * (wl.nt - 1))
         peak, peak_src = hbm_peak()
-        fwd_name = {0: "fwd_step_kernel", 1: "fwd_qres_kernel", 2: "fwd2_kernel", 3: "fwd_t2_kernel"}.get(
+        fwd_name = {0: "fwd_step_kernel", 1: "fwd_qres_kernel", 3: "fwd_t2_kernel", 4: "fwd_qres_cl_kernel"}.get(
             stats["fwd_kernel"], "fwd_step_kernel")
         bwd_name = {0: "bwd_step_kernel", 3: "bwd_t2_kernel"}.get(stats.get("bwd_kernel", 0), "bwd_step_kernel")
         kern = {fwd_name: (fb_alg, fb_bat, f_launch_ms)}

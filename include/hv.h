@@ -220,7 +220,8 @@ typedef struct {
   double  ms_backward;       /* device time of the backward sweeps, last call                 */
   double  ms_total;          /* device time of the whole call                                 */
   int32_t fwd_kernel;        /* forward sweep kernel used: 0 one-wave (fwd_step_kernel), 1 resident-q
-                                (fwd_qres_kernel, Q > 48 MB), 3 two levels per launch (fwd_t2_kernel) */
+                                (fwd_qres_kernel, Q > 48 MB), 3 two levels per launch (fwd_t2_kernel),
+                                4 resident-q with thread-block clusters (fwd_qres_cl_kernel)        */
   int32_t bwd_kernel;        /* adjoint sweep kernel used: 0 bwd_step_kernel, 3 bwd_t2_kernel, -1 none   */
 } hv_stats;
 HV_API int hv_get_stats(const hv_ctx* ctx, hv_stats* out);

@@ -53,8 +53,9 @@ constexpr int kPhiBlocks = 1024;  // residual kernel grid: fixed, so phi's summa
 #ifndef HV_QRES_FG
 #define HV_QRES_FG 6
 #endif
-constexpr int kQresFG = HV_QRES_FG;
-constexpr int kQresOrder = 0;  // fwd_qres_kernel grid order (FwdParams::qorder)  // resident-q forward: Born fields per CTA (6 q_k tiles + 3 stages: 2 CTAs/SM)
+constexpr int kQresFG = HV_QRES_FG;  // resident-q forward: Born fields per CTA (6 q_k tiles + 3 stages: 2 CTAs/SM)
+constexpr int kQresOrder = 0;        // fwd_qres_kernel grid order (FwdParams::qorder)
+constexpr bool kQresClusterDefault = false;  // fwd_qres_cl_kernel for K <= 32
 // Backward CTAs per (tile, field group): the batch's shots are split into this many parts, each summing its
 // imaging terms into its own accumulator copy (finalize adds the copies in a fixed order). 2 halves the last
 // partial wave of the backward grid at the cost of one more RED per point and field per launch; measured on
@@ -409,7 +410,11 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
   // forward sweep kernel (decided here, not inside enqueue_batch: replayed graphs never re-run the lambda)
   bool qres_call = K > 0 && 4.0 * K * g.plane > 48e6;
   if (const char* qe = std::getenv("HV_QRES")) qres_call = K > 0 && std::strcmp(qe, "0") != 0;
-  const int fwd_kernel_used = use_t2 ? 3 : (qres_call ? 1 : 0);
+  // cluster variant (fwd_qres_cl_kernel): up to 8 groups of <= 4 Born fields per tile in one cluster, the
+  // background processed once per tile and shot (K <= 32); HV_QRES_CLUSTER=0/1 overrides
+  bool qcl_call = qres_call && kQresClusterDefault && K <= 32;
+  if (const char* qc = std::getenv("HV_QRES_CLUSTER")) qcl_call = qres_call && K <= 32 && std::strcmp(qc, "0") != 0;
+  const int fwd_kernel_used = use_t2 ? 3 : (qcl_call ? 4 : (qres_call ? 1 : 0));
   // phase 0: forward sweep (+ gather); phase 1: backward sweep. Events may be null (recorded by the caller).
   auto enqueue_batch = [&](int phase, int b0, int Sb, cudaEvent_t e_f0, cudaEvent_t e_f1, cudaEvent_t e_b0,
                            cudaEvent_t e_b1) -> int {
@@ -465,10 +470,26 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
     const dim3 gridf(fwd_grid(ntiles_all * Gf * Sb));
     // resident-q forward (q_k read once per launch) for Q too large for L2: HV_QRES=0/1 overrides (tuning)
     const bool qres = qres_call;
-    fp.qfg = std::min(K > 0 ? K : 1, kQresFG);
-    if (const char* qf = std::getenv("HV_QFG")) fp.qfg = std::max(1, std::min({K > 0 ? K : 1, 16, std::atoi(qf)}));
+    const bool qcl = qcl_call;
+    fp.qfg = qcl ? (K + 7) / 8 : std::min(K > 0 ? K : 1, kQresFG);
+    if (!qcl)
+      if (const char* qf = std::getenv("HV_QFG")) fp.qfg = std::max(1, std::min({K > 0 ? K : 1, 16, std::atoi(qf)}));
     const int Gq = K > 0 ? (K + fp.qfg - 1) / fp.qfg : 1;
-    const int qres_smem = QSTAGES_BYTES + BAR_BYTES + fp.qfg * PT_BYTES;
+    const int qres_smem = QSTAGES_BYTES + BAR_BYTES + fp.qfg * PT_BYTES + (qcl ? 2 * PT_BYTES : 0);
+    cudaLaunchConfig_t qcfg{};
+    cudaLaunchAttribute qattr[1];
+    if (qcl) {
+      qcfg.gridDim = dim3(g.ntx, g.ntz, Gq);
+      qcfg.blockDim = block;
+      qcfg.dynamicSmemBytes = qres_smem;
+      qcfg.stream = c->stream;
+      qattr[0].id = cudaLaunchAttributeClusterDimension;
+      qattr[0].val.clusterDim.x = 1;
+      qattr[0].val.clusterDim.y = 1;
+      qattr[0].val.clusterDim.z = Gq;
+      qcfg.attrs = qattr;
+      qcfg.numAttrs = 1;
+    }
     if (phase == 0 && use_t2) {
       T2Params t2{};
       t2.g = g;
@@ -523,7 +544,9 @@ int run(hv_ctx* c, int want, const float* m_in, const float* dobs_in, int K, con
         fp.n = n;
         fp.s_out = full ? store + (size_t)n * g.iplane : nullptr;
         fp.ring_out = boundary ? ring + (size_t)(n + 1) * ringN : nullptr;
-        if (qres)
+        if (qcl)
+          CU_TRY(cudaLaunchKernelEx(&qcfg, fwd_qres_cl_kernel, map_halo, map_tile, map_q, map_d, fp));
+        else if (qres)
           fwd_qres_kernel<<<dim3(g.ntx * g.ntz * Gq), block, qres_smem, c->stream>>>(map_halo, map_tile, map_q,
                                                                                       map_d, fp);
         else
@@ -973,6 +996,8 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
                            QSTAGES_BYTES + BAR_BYTES + 16 * PT_BYTES) != cudaSuccess ||
       cudaFuncSetAttribute(fwd_t2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t2_fwd_smem_bytes()) !=
           cudaSuccess ||
+      cudaFuncSetAttribute(fwd_qres_cl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           QSTAGES_BYTES + BAR_BYTES + 6 * PT_BYTES) != cudaSuccess ||
       cudaFuncSetAttribute(bwd_t2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t2_bwd_smem_bytes()) !=
           cudaSuccess ||
       cudaFuncSetAttribute(rev_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, REV_SMEM_BYTES) !=

@@ -118,6 +118,23 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// Thread-block clusters: distributed shared memory reads and the cluster-wide barrier.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -699,22 +716,27 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
 // fields) loops over all the batch's shots; the group's q_k tiles are loaded into shared memory once and reused by
 // every shot (q_k is read from DRAM once per launch), the resident CTAs step through the shots in lockstep (halo
 // overlaps are L2 hits). Same paired-fp32 (FFMA2) arithmetic as fwd_step_kernel (bit-identical fields).
-template <bool SP>
+// CL: thread-block-cluster variant (fwd_qres_cl_kernel): the G field groups of a tile form one cluster; only the
+// leader (group 0) processes the background item and publishes L u^n through distributed shared memory (lbuf,
+// double-buffered by shot), so the background halo is loaded and its Laplacian computed once per tile and shot
+// instead of once per group. One cluster barrier per shot.
+template <bool SP, bool CL>
 __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUtensorMap* mt, const CUtensorMap* mq,
                                          const CUtensorMap* md, const FwdParams& p, float* stages, float* qs,
-                                         uint64_t* bars, int bx, int by, int grp) {
+                                         uint64_t* bars, int bx, int by, int grp, float* lbuf = nullptr) {
   const Geo& g = p.g;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * BX + tx;
   const int x0 = bx * TX, z0 = by * TZ;
   const int fb = grp * p.qfg;
   const int nf = max(0, min(p.K, fb + p.qfg) - fb);   // Born fields of this CTA
-  const int nitems = p.S * (1 + nf);                  // per shot: background, then its Born fields
   const int par_n = p.n & 1, par_new = par_n ^ 1;
   const bool leader = (grp == 0) && p.bg_update;
+  const bool has_bg = !CL || grp == 0;                   // this CTA processes the background item
+  const int nitems = p.S * ((has_bg ? 1 : 0) + nf);      // per shot: [background], then its Born fields
   uint64_t* qbar = bars + NSTAGE_Q;
 
-  // producer (thread 0): next item (ps, pt) -> stage
-  int ps = 0, pt = 0, issued = 0;
+  // producer (thread 0): next item (ps, pt) -> stage; pt = 0 is the background item
+  int ps = 0, pt = has_bg ? 0 : 1, issued = 0;
   RingN<NSTAGE_Q> prod;
   auto issue_next = [&]() {
     float* st = stages + prod.stage * STAGE_FLOATS;
@@ -742,7 +764,7 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
 #endif
     prod.advance();
     if (++pt > nf) {
-      pt = 0;
+      pt = has_bg ? 0 : 1;
       ++ps;
     }
     ++issued;
@@ -807,11 +829,16 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
   float2 Lb[RZ][2];
   for (int s = 0; s < p.S; ++s) {
     // ---------------- background u of shot s: L u^n (kept for the Born sources), leader updates u
-    {
+    if (has_bg) {
       const float* st = stages + cons.stage * STAGE_FLOATS;
       mbar_wait(&bars[cons.stage], cons.phase);
       float2 C[RZ][2];
       lap_points_bg(st, tx, ty, Lb, C);
+      if constexpr (CL) {  // publish L u^n for the cluster's other field groups
+#pragma unroll
+        for (int r = 0; r < RZ; ++r)
+          st4(lbuf + (s & 1) * PT_FLOATS + so + r * TX, make_float4(Lb[r][0].x, Lb[r][0].y, Lb[r][1].x, Lb[r][1].y));
+      }
       if (leader) {
         float* dst = p.pool + (static_cast<long long>(s * p.nslot + p.bg_slot) * 2 + par_new) * g.plane;
         float* dD = p.dbuf + static_cast<long long>((p.dplane0 + s) * 2) * g.plane;
@@ -869,6 +896,17 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
         if (re > rb && p.d_bg) sample(st, p.d_bg + (p.dbg_shot0 + s) * data_stride);
       }
       release();
+    }
+    if constexpr (CL) {
+      cluster_sync_all();  // lbuf[s & 1] of the leader is complete (and every CTA is done with shot s - 1's)
+      if (!has_bg) {
+        const uint32_t src = mapa_shared(smem_u32(lbuf + (s & 1) * PT_FLOATS + so), 0);
+#pragma unroll
+        for (int r = 0; r < RZ; ++r) {
+          const float4 v = ld_dsmem4(src + r * TX * 4);
+          Lb[r][0] = lo2(v), Lb[r][1] = hi2(v);
+        }
+      }
     }
     // ---------------- Born fields du_k of shot s: source q_k L u^n
     float* born_base = p.pool + (static_cast<long long>(s * p.nslot + p.born_slot0 + fb) * 2 + par_new) * g.plane;
@@ -931,9 +969,36 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
   }
   const int by = tile / p.g.ntx, bx = tile - by * p.g.ntx;
   if (tile_is_interior(p.g, bx * TX, by * TZ))
-    fwd_qres_body<false>(&mh, &mt, &mq, &md, p, stages, qs, bars, bx, by, grp);
+    fwd_qres_body<false, false>(&mh, &mt, &mq, &md, p, stages, qs, bars, bx, by, grp);
   else
-    fwd_qres_body<true>(&mh, &mt, &mq, &md, p, stages, qs, bars, bx, by, grp);
+    fwd_qres_body<true, false>(&mh, &mt, &mq, &md, p, stages, qs, bars, bx, by, grp);
+}
+
+// Cluster variant: grid (ntx, ntz, G) launched with cluster dimensions (1, 1, G), G <= 8; p.qfg Born fields per
+// group. Shared memory: stages | barriers | q tiles (qfg) | lbuf (2 planes of the tile's L u^n).
+__global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
+    fwd_qres_cl_kernel(const __grid_constant__ CUtensorMap mh, const __grid_constant__ CUtensorMap mt,
+                       const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap md,
+                       const FwdParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stages = reinterpret_cast<float*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + QSTAGES_BYTES);
+  float* qs = reinterpret_cast<float*>(smem_raw + QSTAGES_BYTES + BAR_BYTES);
+  float* lbuf = qs + p.qfg * PT_FLOATS;
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    tma_prefetch_desc(&mh);
+    tma_prefetch_desc(&mt);
+    tma_prefetch_desc(&mq);
+    for (int i = 0; i < NSTAGE_Q + 1; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int bx = blockIdx.x, by = blockIdx.y, grp = blockIdx.z;  // cluster (1, 1, G): rank = group
+  if (tile_is_interior(p.g, bx * TX, by * TZ))
+    fwd_qres_body<false, true>(&mh, &mt, &mq, &md, p, stages, qs, bars, bx, by, grp, lbuf);
+  else
+    fwd_qres_body<true, true>(&mh, &mt, &mq, &md, p, stages, qs, bars, bx, by, grp, lbuf);
+  cluster_sync_all();  // the leader's lbuf must outlive every remote read
 }
 
 // ------------------------------------------------------------------------------------------------ backward

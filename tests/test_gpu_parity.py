@@ -244,6 +244,13 @@ def test_resident_q_forward(hv, ragged, store, monkeypatch):
         out[q] = (s.forward(wl.model), s.hessvec(wl.model, V))
     assert rel_l2(out["1"][0], d) <= TOL and rel_l2(out["1"][1], HV) <= TOL
     assert rel_l2(out["1"][0], out["0"][0]) <= 1e-6 and rel_l2(out["1"][1], out["0"][1]) <= 1e-6
+    # thread-block-cluster variant (experimental, off by default): background once per tile, shared by DSMEM
+    monkeypatch.setenv("HV_QRES", "1")
+    monkeypatch.setenv("HV_QRES_CLUSTER", "1")
+    s = hv.Solver.from_workload(wl, store=store, shot_batch=2)
+    hcl = s.hessvec(wl.model, V)
+    assert s.stats()["fwd_kernel"] == 4
+    assert rel_l2(hcl, HV) <= TOL and rel_l2(hcl, out["1"][1]) <= 1e-6
 
 
 def test_edge_cases(hv):

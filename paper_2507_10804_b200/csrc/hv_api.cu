@@ -907,6 +907,7 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
   g.c0 = (g.W / 4) * 4;
   g.PI = ((g.W + g.nx - g.c0) + 3) / 4 * 4;
   g.plane = (long long)g.Nz * g.P;
+  if (g.plane >= (1LL << 31)) return bad(HV_EINVAL, "padded grid too large (a plane must have < 2^31 points)");
   g.iplane = (long long)g.nz * g.PI;
   const double eta_max = 3.0 * k.v_ref * std::log(1000.0) / (2.0 * k.sponge * k.h);
   g.kc = static_cast<float>(eta_max * k.dt / (2.0 * (double)k.sponge * k.sponge));

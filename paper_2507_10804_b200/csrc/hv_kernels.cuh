@@ -518,7 +518,7 @@ __device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages
   const int I0 = z0 + ty * RZ;
   const int J0 = x0 + tx * 4;
   const int so = ty * RZ * TX + tx * 4;                       // smem offset of this thread's first point
-  const long long go = static_cast<long long>(I0) * g.P + J0;  // plane offset of this thread's first point
+  const int go = I0 * g.P + J0;  // within-plane offset of this thread's first point (plane < 2^31 floats)
   float2 w[RZ][2];  // from the background item's stage (TMA), below
   bool row_ok[RZ];
 #pragma unroll
@@ -557,7 +557,7 @@ __device__ __forceinline__ void fwd_unit(const FwdParams& p, const float* stages
       for (int i = 0; i < 4; ++i)
         if (J0 + i >= g.Nx) v[i] = 0.0f;
     }
-    if (row_ok[r]) st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
+    if (row_ok[r]) st4(dst + (go + r * g.P), make_float4(v[0], v[1], v[2], v[3]));
   };
 
   // ---------------- background u of shot s: L u^n (kept for the Born sources), leader updates u
@@ -780,7 +780,7 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
   const int I0 = z0 + ty * RZ;
   const int J0 = x0 + tx * 4;
   const int so = ty * RZ * TX + tx * 4;                       // smem offset of this thread's first point
-  const long long go = static_cast<long long>(I0) * g.P + J0;  // plane offset of this thread's first point
+  const int go = I0 * g.P + J0;  // within-plane offset of this thread's first point (plane < 2^31 floats)
   float2 w[RZ][2];
 #pragma unroll
   for (int r = 0; r < RZ; ++r) {
@@ -823,7 +823,7 @@ __device__ __forceinline__ void fwd_qres_body(const CUtensorMap* mh, const CUten
       for (int i = 0; i < 4; ++i)
         if (J0 + i >= g.Nx) v[i] = 0.0f;
     }
-    if (row_ok[r]) st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
+    if (row_ok[r]) st4(dst + (go + r * g.P), make_float4(v[0], v[1], v[2], v[3]));
   };
 
   float2 Lb[RZ][2];
@@ -1085,7 +1085,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
   const int I0 = z0 + ty * RZ;
   const int J0 = x0 + tx * 4;
   const int so = ty * RZ * TX + tx * 4;
-  const long long go = static_cast<long long>(I0) * g.P + J0;
+  const int go = I0 * g.P + J0;  // within-plane offset (plane < 2^31 floats)
   const int jc = J0 - g.c0;
 #if HV_BWD_PAIRED
   float2 w2[RZ][2];
@@ -1163,7 +1163,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
             for (int i = 0; i < 4; ++i)
               if (J0 + i >= g.Nx) v[i] = 0.0f;
           }
-          if (row_ok[r]) st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
+          if (row_ok[r]) st4(dst + (go + r * g.P), make_float4(v[0], v[1], v[2], v[3]));
         }
       }
 #pragma unroll
@@ -1196,7 +1196,7 @@ __device__ __forceinline__ void bwd_body(const CUtensorMap* mh, const CUtensorMa
             for (int i = 0; i < 4; ++i)
               if (J0 + i >= g.Nx) v[i] = 0.0f;
           }
-          if (row_ok[r]) st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
+          if (row_ok[r]) st4(dst + (go + r * g.P), make_float4(v[0], v[1], v[2], v[3]));
         }
       }
       // zero-lag imaging, summed over the batch's shots in registers: acc += s^j * lambda^{j+1}
@@ -1313,7 +1313,7 @@ __device__ __forceinline__ void rev_body(const CUtensorMap* mh, const CUtensorMa
   const int I0 = z0 + ty * RZ;
   const int J0 = x0 + tx * 4;
   const int so = ty * RZ * TX + tx * 4;
-  const long long go = static_cast<long long>(I0) * g.P + J0;
+  const int go = I0 * g.P + J0;  // within-plane offset (plane < 2^31 floats)
   float w[RZ][4];
   int rq[RZ][4];       // ring index (>= 0), interior (-1), or neither (-2)
 #pragma unroll
@@ -1356,11 +1356,11 @@ __device__ __forceinline__ void rev_body(const CUtensorMap* mh, const CUtensorMa
         if (SP && rq[r][i] >= 0) v[i] = p.ring_in[s * p.ring_shot_stride + rq[r][i]];
       }
       if (!SP) {
-        st4(dst + go + static_cast<long long>(r) * g.P, make_float4(v[0], v[1], v[2], v[3]));
+        st4(dst + (go + r * g.P), make_float4(v[0], v[1], v[2], v[3]));
       } else if (I0 + r < g.Nz) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          if (rq[r][i] != -2) dst[go + static_cast<long long>(r) * g.P + i] = v[i];
+          if (rq[r][i] != -2) dst[(go + r * g.P) + i] = v[i];
       }
       // s^j on the interior
       const int iz = I0 + r - g.W;

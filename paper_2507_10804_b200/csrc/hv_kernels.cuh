@@ -196,6 +196,21 @@ __device__ __forceinline__ void lap_points_w(const float* __restrict__ t, int tx
   float4 zw[RZ + 2 * R];
 #pragma unroll
   for (int k = 0; k < RZ + 2 * R; ++k) zw[k] = ld4(t + (ty * RZ + k) * W + col);
+  // z differences shared by the thread's RZ rows (the d = 1, 2 terms below): f1[k] = z[k + 1] - z[k] for
+  // k = R - 1 .. R + RZ - 1, f2[k] = z[k + 2] - z[k] for k = R - 2 .. R + RZ - 1 (index k - (R - 2) in the arrays).
+  // (z[c+d] - z[c]) + (z[c-d] - z[c]) = f_d[c] - f_d[c-d] exactly (negating a rounded difference is exact), so the
+  // bits are those of the per-row form.
+  float2 f1[RZ + 2][2], f2[RZ + 2][2];
+  if constexpr (DIFF) {
+#pragma unroll
+    for (int k = 0; k < RZ + 2; ++k)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = k + R - 2;
+        if (k >= 1) f1[k][h] = sub2(half2of(zw[a + 1], h), half2of(zw[a], h));
+        f2[k][h] = sub2(half2of(zw[a + 2], h), half2of(zw[a], h));
+      }
+  }
 #pragma unroll
   for (int r = 0; r < RZ; ++r) {
     const float* row = t + (ty * RZ + r + R) * W + tx * 4;
@@ -228,21 +243,30 @@ __device__ __forceinline__ void lap_points_w(const float* __restrict__ t, int tx
     float e[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) e[k] = __fsub_rn(xs[k + 4], xs[k + 3]);
+    // d = 2 differences of register-aligned pairs, shared by the two column pairs: gx[m] = x[2m + 4 .. 2m + 5] -
+    // x[2m + 2 .. 2m + 3]
+    float2 gx[3];
+#pragma unroll
+    for (int m = 0; m < 3; ++m)
+      gx[m] = sub2(make_float2(xs[2 * m + 4], xs[2 * m + 5]), make_float2(xs[2 * m + 2], xs[2 * m + 3]));
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int i = 2 * h;
       auto P = [&](int k) { return make_float2(xs[k + i], xs[k + i + 1]); };
       auto Z = [&](int k) { return half2of(zw[r + k], h); };
       const float2 ctr = P(4);
-      // (x+d - c) + (x-d - c): even d reads register-aligned pairs (FADD2); odd d straddles the float4s, so the
-      // differences are scalar FADDs (same roundings) written straight into the result pair
+      // (x+d - c) + (x-d - c) as differences of shared first differences (d = 1: scalar e, the pairs straddle the
+      // float4s; d = 2: the aligned pairs gx); d = 3 straddles too and is not shared
       auto DX = [&](int d) {
-        if (d % 2 == 0) return add2(sub2(P(4 + d), ctr), sub2(P(4 - d), ctr));
+        if (d == 2) return sub2(gx[h + 1], gx[h]);
         if (d == 1) return make_float2(__fsub_rn(e[i + 1], e[i]), __fsub_rn(e[i + 2], e[i + 1]));
         return make_float2(__fadd_rn(__fsub_rn(xs[4 + d + i], xs[4 + i]), __fsub_rn(xs[4 - d + i], xs[4 + i])),
                            __fadd_rn(__fsub_rn(xs[5 + d + i], xs[5 + i]), __fsub_rn(xs[5 - d + i], xs[5 + i])));
       };
-      auto DZ = [&](int d) { return add2(sub2(Z(4 + d), ctr), sub2(Z(4 - d), ctr)); };
+      auto DZ = [&](int d) {
+        if (d == 1) return sub2(f1[r + 2][h], f1[r + 1][h]);
+        return sub2(f2[r + 2][h], f2[r][h]);
+      };
       // plain pair sums for the small outer weights (|a3|, |a4| <= 0.025): their rounding is 60x below the
       // first two terms', which is where the cancellation happened
       auto X = [&](int d) {

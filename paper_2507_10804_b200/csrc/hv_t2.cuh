@@ -31,9 +31,9 @@ namespace hvk {
 constexpr int T2_OX = OX, T2_OZ = OZ;                      // output tile (level n+2): 56 x 56
 constexpr int T2_MX = T2_OX + 2 * R, T2_MZ = T2_OZ + 2 * R;  // mid region (level n+1): 64 x 64
 constexpr int T2_IX = T2_MX + 2 * R, T2_IZ = T2_MZ + 2 * R;  // input halo box (level n): 72 x 72
-constexpr int T2_BY = T2_MZ / RZ;                          // 32 thread rows (2 rows each)
+constexpr int T2_BY = T2_MZ / RZ;                          // thread rows (RZ rows each)
 constexpr int T2_NT = BX * T2_BY;                          // 512 threads
-constexpr int T2_MINB = T2_NT <= 256 ? 2 : 1;              // resident CTAs per SM the registers are sized for
+constexpr int T2_MINB = T2_NT * RZ / 2 <= 256 ? 2 : 1;     // resident CTAs per SM the registers are sized for
 constexpr int T2_IN_FLOATS = T2_IX * T2_IZ;
 constexpr int T2_MID_FLOATS = T2_MX * T2_MZ;
 constexpr int T2_STAGE_FLOATS = T2_IN_FLOATS + T2_MID_FLOATS;  // halo of level n + level n-1 on the mid region

@@ -988,20 +988,23 @@ int hv_create(const hv_config* cfg, hv_ctx** out) {
     return HV_ECUDA;
   }
   c->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  // opt-in shared memory per CTA (227 KB on sm_100); the tile-size knobs (HV_TZ) can ask for more than a kernel
+  // variant will ever be launched with
+  auto smem_cap = [](int b) { return std::min(b, 227 * 1024); };
   if (cudaFuncSetAttribute(fwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           fwd_smem_bytes(FWD_FG_MAX)) !=
+                           smem_cap(fwd_smem_bytes(FWD_FG_MAX))) !=
           cudaSuccess ||
-      cudaFuncSetAttribute(bwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_SMEM_BYTES) !=
+      cudaFuncSetAttribute(bwd_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap(BWD_SMEM_BYTES)) !=
           cudaSuccess ||
       cudaFuncSetAttribute(fwd_qres_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           QSTAGES_BYTES + BAR_BYTES + 16 * PT_BYTES) != cudaSuccess ||
-      cudaFuncSetAttribute(fwd_t2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t2_fwd_smem_bytes()) !=
+                           smem_cap(QSTAGES_BYTES + BAR_BYTES + 16 * PT_BYTES)) != cudaSuccess ||
+      cudaFuncSetAttribute(fwd_t2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap(t2_fwd_smem_bytes())) !=
           cudaSuccess ||
       cudaFuncSetAttribute(fwd_qres_cl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           QSTAGES_BYTES + BAR_BYTES + 6 * PT_BYTES) != cudaSuccess ||
-      cudaFuncSetAttribute(bwd_t2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, t2_bwd_smem_bytes()) !=
+                           smem_cap(QSTAGES_BYTES + BAR_BYTES + 6 * PT_BYTES)) != cudaSuccess ||
+      cudaFuncSetAttribute(bwd_t2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap(t2_bwd_smem_bytes())) !=
           cudaSuccess ||
-      cudaFuncSetAttribute(rev_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, REV_SMEM_BYTES) !=
+      cudaFuncSetAttribute(rev_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap(REV_SMEM_BYTES)) !=
           cudaSuccess) {
     cudaGetLastError();
     hv_destroy(c);

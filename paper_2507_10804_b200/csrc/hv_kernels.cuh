@@ -359,7 +359,8 @@ struct FwdParams {
   float* dbuf;
   int dplane0;
   int qorder;             // fwd_qres_kernel linear grid order: 0 = tiles (x, then z) fastest, group slowest;
-                          // 1 = group fastest (the groups of a tile share its background halo in L2)
+                          // 1 = group fastest (the groups of a tile share its background halo in L2);
+                          // q >= 2: blocks of q groups, group fastest within a block
 };
 
 // Per-point damping of this thread's points (SP: the tile touches the sponge): (1 - c) and 1 / (1 + c), as
@@ -988,6 +989,10 @@ __global__ void __launch_bounds__(NTHREADS, HV_FWD_MINB)
   int grp, tile;
   if (p.qorder == 1) {
     grp = blockIdx.x % G, tile = blockIdx.x / G;
+  } else if (p.qorder >= 2) {  // blocks of qorder groups, group fastest within a block: (block, tile, group)
+    const int blk = blockIdx.x / (p.qorder * ntl), base = blk * p.qorder;
+    const int gs = min(p.qorder, G - base), rem = blockIdx.x - blk * p.qorder * ntl;
+    tile = rem / gs, grp = base + (rem - tile * gs);
   } else {
     grp = blockIdx.x / ntl, tile = blockIdx.x - grp * ntl;
   }

@@ -141,9 +141,14 @@ int plan_call(hv_ctx* c, int want, int K, int nloc, Plan* pl) {
   }
   double budget = c->cfg.mem_budget ? static_cast<double>(c->cfg.mem_budget)
                                     : 0.9 * (static_cast<double>(freeb) + held);
-  // T = 2 forward (fwd_t2_kernel) for FULL-store and forward-only calls; HV_T2=0/1 overrides the default
+  // T = 2 forward (fwd_t2_kernel) for FULL-store and forward-only calls; HV_T2=0/1 overrides the default.
+  // Default: forward-only calls (hv_forward / hv_forward_shot / hv_misfit: background only, K = 0) on grids with at
+  // least one T = 2 tile per SM. There the single-step launch is latency-bound (0.26 GB per cfg 3 level in 86 us)
+  // and two levels per pass win: cfg 3 misfit 85.6 -> 69.8 us per level; on small grids (cfg 1:
+  // 95 tiles) the T = 2 grid is too small to fill the GPU and loses (12.8 vs 27.4 us).
   const char* t2 = std::getenv("HV_T2");
-  const bool t2_on = t2 ? std::strcmp(t2, "0") != 0 : kTwoStepDefault;
+  const bool t2_fwd_only = K == 0 && !adjoint && static_cast<long long>(g.ntx2) * g.ntz2 >= c->nsm;
+  const bool t2_on = t2 ? std::strcmp(t2, "0") != 0 : (kTwoStepDefault || t2_fwd_only);
   // shared (not per shot): Q, W2, imgc, rec coef, staging of V/HV/m
   const double shared = F4 * (static_cast<double>(K) * g.plane * 2 + g.plane + g.iplane + 4.0 * K * g.nz * g.nx +
                               2.0 * g.nz * g.nx + (double)kBwdSplit * pl->nacc * g.plane) + (1 << 20);

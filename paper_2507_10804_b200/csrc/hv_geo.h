@@ -71,9 +71,11 @@ constexpr int REV_SMEM_BYTES = STAGES_BYTES + BAR_BYTES;  // BOUNDARY reverse ke
 // T = 2 forward kernel (hv_t2.cuh): OX x OZ output tiles, level n+1 on the (OX + 2R) x (OZ + 2R) mid region
 constexpr int OX = 56;
 #ifndef HV_T2_OZ
-#define HV_T2_OZ 56
+#define HV_T2_OZ 24
 #endif
-constexpr int OZ = HV_T2_OZ;  // 56 (512-thread CTAs, 1 per SM) or 24 (256-thread CTAs, 2 per SM)
+// 24: 32-row mid region = 8 thread rows of 4 -> 128-thread CTAs, 2 per SM (the forward-only default path, the
+// fastest measured: 69.8 vs 79.2 us per cfg 3 misfit level with 56); 56: 256-thread CTAs, 1 per SM
+constexpr int OZ = HV_T2_OZ;
 
 
 struct Geo {

@@ -106,6 +106,7 @@ def test_cfg2_forward_full_nt(hv):
     wl = W.config(2)
     s = hv.Solver.from_workload(wl, src_begin=31, src_end=32)
     d_m = s.forward_shot(wl.model, 31)
+    assert s.stats()["fwd_kernel"] == 3   # forward-only on this grid: the T = 2 forward (two levels per launch)
     ref_m = _gold("cfg2_s31_d_m.npz").astype(np.float64)
     assert rel_l2(d_m, ref_m) <= TOL, rel_l2(d_m, ref_m)
     d_t = s.forward_shot(wl.model_true, 31)

@@ -270,6 +270,29 @@ def test_edge_cases(hv):
     assert rel_l2(s.hessvec(wl.model, V), ref.hessvec(list(V.astype(np.float64)))) <= TOL
 
 
+def test_forward_only_t2_default(hv, monkeypatch):
+    """Forward-only calls on a grid with at least one T = 2 tile per SM (the cfg 3 grid) run the T = 2 forward by
+    default; d and the misfit agree with the single-step kernels (HV_T2=0) to rounding (the increment-form
+    background makes isolated 1-ulp differences, as in test_t2_kernels_match_single_step) and with the gradient's
+    phi (single-step forward)."""
+    wl = W.config(3).subset(shots=range(3), nt=300)
+    monkeypatch.delenv("HV_T2", raising=False)
+    s = hv.Solver.from_workload(wl)
+    d = s.forward(wl.model)
+    assert s.stats()["fwd_kernel"] == 3
+    m0 = (0.98 * wl.model).astype(np.float32)
+    phi = s.misfit(m0, d)
+    assert s.stats()["fwd_kernel"] == 3
+    phig, _ = s.gradient(m0, d)
+    assert phi > 0 and abs(phi - phig) <= 1e-6 * phig
+    monkeypatch.setenv("HV_T2", "0")
+    s0 = hv.Solver.from_workload(wl)
+    d0 = s0.forward(wl.model)
+    assert s0.stats()["fwd_kernel"] != 3
+    assert rel_l2(d, d0) <= 1e-6
+    assert abs(s0.misfit(m0, d) - phi) <= 1e-6 * phi
+
+
 def test_duplicate_receivers(hv):
     """Two receivers on one node (and one on a tile corner): the adjoint's R^T injects both (receiver chain of the
     backward kernel's per-tile map) and the gradient and H·v match the oracle."""
